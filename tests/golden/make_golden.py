@@ -1,0 +1,238 @@
+"""Generate golden vectors by running the REAL reference (kbesolve 0.1.0).
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes ``tests/golden/*.npz``.  Every fixture stores its inputs alongside
+the reference outputs, so tests never need the reference (or a particular
+numpy RNG) at run time.  The reference is deterministic bitwise (SURVEY
+probe P5), so re-running this script reproduces the same bytes.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.environ.get("KBE_REFERENCE_SRC", "/root/reference/pkg/src"))
+
+import kbesolve as kb  # noqa: E402
+from kbesolve.state import mirror_frontier  # noqa: E402
+
+
+def _save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
+
+
+def sigma_fixture():
+    out = {}
+    for n_k in (2, 4, 8, 16, 32, 64):
+        grid = kb.build_kgrid(n_k)
+        rng = np.random.default_rng(100 + n_k)
+        shape = (n_k, 2, 2, 5)
+        gl = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        gg = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        u1 = np.linspace(0.4, 1.2, 5)
+        u2 = 0.7
+        pol = kb.polarizability(gl, gg, grid)
+        s1 = kb.sigma_first(pol, gl, u1, u2, grid)
+        s2 = kb.sigma_second(gl, gg, u1, u2, grid)
+        out[f"gl_{n_k}"] = gl
+        out[f"gg_{n_k}"] = gg
+        out[f"u1_{n_k}"] = u1
+        out[f"u2_{n_k}"] = np.array(u2)
+        out[f"pol_{n_k}"] = pol
+        out[f"s1_{n_k}"] = s1
+        out[f"s2_{n_k}"] = s2
+        out[f"sigma_{n_k}"] = kb.sigma_slice(gl, gg, u1, u2, grid)
+        # k-range (shard) evaluation
+        out[f"sigma_shard_{n_k}"] = kb.sigma_slice(gl, gg, u1, u2, grid, (n_k // 2, n_k))
+    _save("sigma.npz", **out)
+
+
+def _random_history(n_k, cap, frontier, seed, dt):
+    """Random G and Sigma histories with the reference's mirror structure."""
+    grid = kb.build_kgrid(n_k)
+    rng = np.random.default_rng(seed)
+    state = kb.init_state(grid, cap, dt)
+    shape = state.lesser.shape
+    state.lesser[:] = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    state.greater[:] = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    state.frontier = frontier
+    for n in range(frontier + 1):
+        mirror_frontier(state, n)
+    sigma = kb.init_sigma_history(n_k, cap)
+    sigma.lesser[:] = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    sigma.greater[:] = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    for n in range(1, frontier + 1):
+        # evaluate_sigma_batched stores Sigma< on columns, Sigma> on rows and
+        # mirrors the rest (selfenergy.py:317-325)
+        sigma.lesser[:, :, :, n, :n] = -np.conj(np.swapaxes(sigma.lesser[:, :, :, :n, n], 1, 2))
+        sigma.greater[:, :, :, :n, n] = -np.conj(np.swapaxes(sigma.greater[:, :, :, n, :n], 1, 2))
+    return grid, state, sigma
+
+
+def collision_fixture():
+    out = {}
+    n_k, cap, frontier, dt = 4, 9, 8, 0.05
+    grid, state, sigma = _random_history(n_k, cap, frontier, 200, dt)
+    out["GL"] = state.lesser
+    out["GG"] = state.greater
+    out["SL"] = sigma.lesser
+    out["SG"] = sigma.greater
+    out["dt"] = np.array(dt)
+    for kind in ("trapezoid", "simpson"):
+        for mode in ("as-printed", "langreth"):
+            for n in (0, 1, 2, 5, 8):
+                c = kb.collision_frontier(state, sigma, n, kb.QuadratureRule(kind), None, mode)
+                tag = f"{kind}_{mode}_{n}"
+                out[f"lr_{tag}"] = c.lesser_row
+                out[f"gr_{tag}"] = c.greater_row
+                out[f"lc_{tag}"] = c.lesser_col
+                out[f"gc_{tag}"] = c.greater_col
+    # per-pair oracle entries (collision.py:115-138)
+    out["pair_lesser_k1_i5_l2"] = kb.collision_lesser(state, sigma, 1, 5, 2)
+    out["pair_greater_k2_i3_l6"] = kb.collision_greater(state, sigma, 2, 3, 6)
+    for n in (0, 3, 8):
+        w = kb.quadrature_weights(n, dt, "simpson")
+        out[f"wsimp_{n}"] = w
+        out[f"wtrap_{n}"] = kb.quadrature_weights(n, dt, "trapezoid")
+    for n in (1, 2, 7, 10):
+        out[f"wsimp_{n}"] = kb.quadrature_weights(n, dt, "simpson")
+        out[f"wtrap_{n}"] = kb.quadrature_weights(n, dt, "trapezoid")
+    _save("collision.npz", **out)
+
+
+def sigma_batched_fixture():
+    out = {}
+    n_k, cap, frontier, dt = 8, 7, 6, 0.05
+    grid, state, _ = _random_history(n_k, cap, frontier, 300, dt)
+    u = np.linspace(0.4, 0.9, cap + 1)
+    out["GL"] = state.lesser
+    out["GG"] = state.greater
+    out["u"] = u
+    for n in (0, 3, 6):
+        sig = kb.init_sigma_history(n_k, cap)
+        kb.evaluate_sigma_batched(state, sig, n, grid, u)
+        out[f"SL_{n}"] = sig.lesser
+        out[f"SG_{n}"] = sig.greater
+    _save("sigma_batched.npz", **out)
+
+
+def _run_fixture(name, n_k, model, step_cfg, full=False, rows_every=None, schedule=None):
+    grid = kb.build_kgrid(n_k)
+    t0 = time.time()
+    drv = kb.PropagationDriver(grid, model, step_cfg, schedule)
+    reps = drv.run()
+    el = time.time() - t0
+    N = step_cfg.n_steps
+    st = drv.state
+    idx = np.arange(N + 1)
+    out = {
+        "n_k": np.array(n_k),
+        "dt": np.array(step_cfg.dt),
+        "n_steps": np.array(N),
+        "eps": np.array(step_cfg.eps),
+        "max_iter": np.array(step_cfg.max_iter),
+        "quadrature": np.array(step_cfg.quadrature),
+        "limit_mode": np.array(step_cfg.limit_mode),
+        "band_gap": np.array(model.band_gap),
+        "hopping": np.array(model.hopping),
+        "u_protocol": np.asarray(model.u_protocol, dtype=float),
+        "pulse_intensity": np.array(model.pulse_intensity),
+        "pulse_center": np.array(model.pulse_center),
+        "dipole": np.array(complex(model.dipole)),
+        "hf_mode": np.array(model.hf_mode),
+        "iterations": np.array([r.iterations for r in reps]),
+        "residual": np.array([r.residual for r in reps]),
+        "converged": np.array([r.converged for r in reps]),
+        "drift": np.array([r.anticommutation_drift for r in reps]),
+        "density": np.array([r.density for r in reps]),
+        "diag_lesser": st.lesser[:, :, :, idx, idx],
+        "diag_greater": st.greater[:, :, :, idx, idx],
+        "final_row_lesser": st.lesser[:, :, :, N, :],
+        "final_col_greater": st.greater[:, :, :, :, N],
+        "ref_seconds": np.array(el),
+    }
+    if model.eps_c_table is not None:
+        out["eps_c_table"] = np.asarray(model.eps_c_table)
+        out["eps_v_table"] = np.asarray(model.eps_v_table)
+    if full:
+        out["GL"] = st.lesser
+        out["GG"] = st.greater
+        out["SL"] = drv.sigma.lesser
+        out["SG"] = drv.sigma.greater
+    if rows_every:
+        steps = np.arange(0, N + 1, rows_every)
+        out["row_steps"] = steps
+        out["rows_lesser"] = np.stack([st.lesser[:, :, :, s, :] for s in steps])
+        out["cols_greater"] = np.stack([st.greater[:, :, :, :, s] for s in steps])
+    _save(name, **out)
+    print(f"  {name}: reference run {el:.1f}s, iterations {np.bincount(out['iterations'])}")
+
+
+def trajectory_fixtures():
+    # cfg1: the Hubbard dimer exactly as BASELINE.json names it
+    _run_fixture(
+        "traj_dimer.npz", 2,
+        kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.5),
+        kb.StepConfig(dt=0.02, n_steps=200), rows_every=25,
+    )
+    # small full-history run with an early pulse (every stored array pinned)
+    _run_fixture(
+        "traj_nk4_full.npz", 4,
+        kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.1),
+        kb.StepConfig(dt=0.02, n_steps=30), full=True,
+    )
+    # options: Hartree-Fock, Simpson, Langreth limit, time-dependent U
+    u_ramp = np.linspace(0.5, 1.5, 21)
+    _run_fixture(
+        "traj_hf.npz", 4,
+        kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.3, pulse_center=0.1, hf_mode="on"),
+        kb.StepConfig(dt=0.02, n_steps=20), full=True,
+    )
+    _run_fixture(
+        "traj_simpson.npz", 4,
+        kb.ModelConfig(u_protocol=u_ramp, pulse_intensity=0.3, pulse_center=0.1),
+        kb.StepConfig(dt=0.02, n_steps=20, quadrature="simpson"), full=True,
+    )
+    _run_fixture(
+        "traj_langreth.npz", 4,
+        kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.3, pulse_center=0.1, dipole=0.8 + 0.3j),
+        kb.StepConfig(dt=0.02, n_steps=20, limit_mode="langreth"), full=True,
+    )
+    # cfg2 prefix (n_k=16), past the pulse at step 25
+    _run_fixture(
+        "traj_nk16.npz", 16,
+        kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.5),
+        kb.StepConfig(dt=0.02, n_steps=40), rows_every=10,
+    )
+    # cfg3 synthetic tables, prefix with the pulse moved early
+    rng = np.random.default_rng(7)
+    eps_c = 1.0 + rng.uniform(0.0, 1.0, 64)
+    u_tab = 1.0 + 0.1 * rng.standard_normal(1001)
+    _run_fixture(
+        "traj_nk64_synth.npz", 64,
+        kb.ModelConfig(u_protocol=u_tab, pulse_intensity=0.2, pulse_center=0.1,
+                       eps_c_table=eps_c, eps_v_table=-eps_c),
+        kb.StepConfig(dt=0.02, n_steps=12, memory_budget=4 * 1024**3), rows_every=4,
+        schedule=kb.Schedule(n_shards=8),
+    )
+    # free evolution (U = 0, no pulse): analytic known answer
+    _run_fixture(
+        "traj_free.npz", 16, kb.ModelConfig(),
+        kb.StepConfig(dt=0.02, n_steps=100), rows_every=50,
+    )
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["sigma", "collision", "sigma_batched", "trajectory"]
+    for w in which:
+        globals()[f"{w}_fixture" if w != "trajectory" else "trajectory_fixtures"]()
