@@ -1,0 +1,175 @@
+/*
+ * kbe200 — C ABI of the B200 (sm_100a) two-time Kadanoff–Baym propagator.
+ *
+ * The reference (kbesolve 0.1.0, pure Python/numpy) has no FFI layer; its
+ * boundary is the Python API re-exported by pkg/src/kbesolve/__init__.py:3-66.
+ * Every entry point below replaces one reference operator on the step path
+ * (file:line cited per function).  The Python package
+ * paper_2505_19467_b200 binds these with ctypes and keeps
+ * the reference's names, argument meaning and exception types.
+ *
+ * Conventions
+ *   - complex128 values are `double[2]` pairs (re, im), passed as void*.
+ *   - every pointer argument is DEVICE memory unless the name ends in _host.
+ *   - every call is asynchronous on the given CUDA stream (`void* stream`,
+ *     a cudaStream_t; NULL = legacy default stream) and returns an int status
+ *     (KBE_OK = 0); kbe_last_error() describes the last failure.
+ *   - nothing allocates device memory: all buffers are owned by the caller
+ *     (the Python driver allocates them once, at construction).
+ *
+ * Packed, time-sliced history layout (one per function; G and Sigma):
+ *   hist[k_local][ slice_offset(s) + c * plane_len(s) + b ]    complex128
+ *   slice s holds, for b = 0..s, eight complex planes c:
+ *     c = 0..3  the LOWER-triangle block X(t_s, t_b)   (row-major 2x2)
+ *     c = 4..7  the UPPER-triangle block Y(t_b, t_s)
+ *   G:     lower = G<  (advanced along rows),    upper = G>  (along columns)
+ *   Sigma: lower = S>  (selfenergy.py:318),      upper = S<  (selfenergy.py:317)
+ *   Everything else follows from X(t',t) = -X(t,t')^dagger (state.py:95-109).
+ *   plane_len(s) = 8*ceil((s+1)/8) so that every plane starts 128-byte aligned.
+ */
+#ifndef KBE200_H
+#define KBE200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KBE_OK 0
+#define KBE_ERR_ARG 1
+#define KBE_ERR_CUDA 2
+#define KBE_ERR_UNSUPPORTED 3
+
+#define KBE_MAX_ITER 16      /* StepConfig.max_iter ceiling on the device path */
+#define KBE_TILE_B 128       /* collision tile: history points per CTA        */
+#define KBE_TILE_S 64        /* collision tile: time slices per CTA           */
+#define KBE_REPORT_W 24      /* doubles per StepReport row (8 + KBE_MAX_ITER)  */
+
+/* Report row layout (doubles):
+ *  0 step, 1 iterations, 2 residual, 3 converged, 4 anticommutation drift
+ *  (max over local k), 5 sum over local k of n_v + n_c, 6 non-finite flag,
+ *  7 reserved, 8.. residual history (KBE_MAX_ITER entries). */
+
+/* Everything a step needs.  Scalars mirror StepConfig / ModelConfig
+ * (propagator.py:44-52, model.py:27-37); pointers are caller-owned device
+ * buffers sized by the kbe_*_bytes / kbe_tri_size helpers. */
+typedef struct kbe_problem {
+    int32_t n_k;          /* global k-point count (even, kgrid.py:30-39)          */
+    int32_t k_lo;         /* local k range [k_lo, k_hi) of this rank               */
+    int32_t k_hi;
+    int32_t n_steps;      /* capacity N: slices 0..N                               */
+    int32_t quad;         /* 0 trapezoid, 1 simpson (collision.py:31-61)           */
+    int32_t limit_mode;   /* 0 as-printed (1 langreth: not on the device path yet) */
+    int32_t hf;           /* hf_mode == "on"                                       */
+    int32_t max_iter;     /* corrector cap, <= KBE_MAX_ITER                         */
+    int32_t interacting;  /* any(U != 0): Sigma is evaluated (propagator.py:265)   */
+    int32_t nbb;          /* partial-sum columns per output: ceil((N+1)/TILE_B)    */
+    int32_t nsb;          /* partial-sum columns per output: ceil((N+1)/TILE_S)    */
+    int32_t pad0;
+    double dt, eps, dipole_re, dipole_im;
+    int64_t tri;          /* complex elements per k of one packed history          */
+    void* g_hist;         /* [k_local][tri]                                        */
+    void* s_hist;         /* [k_local][tri]                                        */
+    const double* eps_v;  /* [n_k] band tables (model.py:71-85), global k          */
+    const double* eps_c;
+    const double* u_table;/* [N+1] U on the grid (model.py:46-56)                  */
+    const double* u_mid;  /* [N+1] U at the step-n midpoint (model.py:59-68)       */
+    const double* amp;    /* [N+1] pulse amplitude at the step-n midpoint (88-103) */
+    void* row_part;       /* [k_local][N+1][nbb][4] complex: row-collision partials*/
+    void* col_part;       /* [k_local][N+1][nsb][4]                                */
+    void* gc_part;        /* [k_local][N+1][nbb][4]: column-collision partials     */
+    void* lr_old;         /* [k_local][N+1][4]: I<(t_{n-1}, t_l) kept for the step */
+    void* col_old;        /* [k_local][N+1][4]: I>(t_j, t_{n-1}) kept for the step */
+    void* front_send;     /* NULL (1 rank) or [k_local][8][plane_len(N)]            */
+    void* front_all;      /* NULL (1 rank) or [n_k][8][plane_len(N)] (allgathered)  */
+    void* ctl;            /* kbe_ctl_bytes() of device control state               */
+    double* reports;      /* [N+1][KBE_REPORT_W]                                   */
+} kbe_problem;
+
+/* ---- layout helpers (host-callable, no device work) ---------------------- */
+int      kbe_abi_version(void);
+int64_t  kbe_plane_len(int32_t s);
+int64_t  kbe_slice_offset(int32_t s);              /* in complex elements      */
+int64_t  kbe_tri_size(int32_t n_steps);            /* complex elements per k    */
+int64_t  kbe_ctl_bytes(void);
+int64_t  kbe_sizeof_problem(void);
+const char* kbe_last_error(void);
+
+/* ---- state (state.py) --------------------------------------------------- */
+/* init_state ground state (state.py:56-87): zero both histories, then
+ * G<(0,0) = i diag(1,0), G>(0,0) = -i diag(0,1) per local k; resets ctl. */
+int kbe_init_history(const kbe_problem* p, void* stream);
+
+/* ---- Sigma (selfenergy.py) ---------------------------------------------- */
+/* evaluate_sigma_batched (selfenergy.py:261-325): both components of the
+ * second-Born Sigma on the step-n frontier, all n+1 pairs, local k, one
+ * launch; writes Sigma slice n.  `it` >= 1 makes the call a no-op once the
+ * corrector has converged (device-side convergence, see kbe_update). */
+int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream);
+
+/* sigma_slice / polarizability / sigma_first / sigma_second
+ * (selfenergy.py:59-236) on batch-last (n_k,2,2,nb) buffers.  Any of
+ * pol_out, s1_out, s2_out, sigma_out may be NULL.  If pol_in is non-NULL it
+ * replaces the computed polarizability in the first term (sigma_first's pol
+ * argument).  u1, u2: [nb] doubles.  Outputs cover k in [k_lo, k_hi)
+ * (pol_out always covers all n_k). */
+int kbe_sigma_slice(int32_t n_k, int32_t nb, const void* g_primary, const void* g_reversed,
+                    const double* u1, const double* u2, int32_t k_lo, int32_t k_hi,
+                    const void* pol_in, void* pol_out, void* s1_out, void* s2_out,
+                    void* sigma_out, void* stream);
+
+/* ---- collision integrals (collision.py) ---------------------------------- */
+/* collision_frontier (collision.py:228-277) at step n into the partial-sum
+ * workspace: row sums over the Sigma history triangle (slices 0..n) and the
+ * column sums over the G history triangle (slices 0..n-1). */
+int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream);
+
+/* Reduce the partials of the last kbe_collision_frontier(n) into the four
+ * CollisionSlice arrays (collision.py:165-176), local k, batch-last:
+ * lesser_row/greater_row (k_local,2,2,n+1), lesser_col/greater_col (k_local,2,2,n). */
+int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void* greater_row,
+                        void* lesser_col, void* greater_col, void* stream);
+
+/* ---- predictor / corrector (propagator.py) -------------------------------- */
+/* phase 0: predict_frontier + _write_frontier (propagator.py:138-163, 208-212)
+ * phase 1: correct_frontier + _frontier_residual + _write_frontier
+ *          (propagator.py:166-220), corrector iteration `it` (0-based).
+ * The Cayley propagator (propagator.py:77-94) is built in-kernel from
+ * h(k; t_{n-1/2}) (model.py:123-152). */
+int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
+
+/* k-mean of rho for hf_mode="on" (model.py:106-120): phase 0 uses
+ * rho(t_{n-1}), phase 1 uses (rho(t_{n-1}) + rho(t_n))/2.  Local k sum;
+ * the caller all-reduces across ranks before dividing (kbe_hf_finalize). */
+int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
+
+/* End of step n: observables_at / anticommutation_drift (state.py:125-137),
+ * _frontier_finite (propagator.py:223-226), StepReport row into reports[n].
+ * A non-finite frontier poisons the device state: later calls are no-ops. */
+int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream);
+
+/* One whole PropagationDriver.step() (propagator.py:316-382) on one rank:
+ * Sigma(n-1), I(n-1), predictor, max_iter x (Sigma(n), I(n), corrector), finish. */
+int kbe_step(const kbe_problem* p, int32_t n, void* stream);
+
+/* Steps n_first..n_last (inclusive) back to back (PropagationDriver.run,
+ * propagator.py:384-392).  use_graph != 0 replays one captured CUDA graph per
+ * step shape. */
+int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream);
+
+/* ---- layout conversion (TwoTimeGF / SigmaHistory accessors) -------------- */
+/* Rebuild the reference layout (k_local,2,2,N+1,N+1) of one function from the
+ * packed history: which = 0 -> lower-stored (G<, S>), 1 -> upper-stored (G>, S<).
+ * Entries beyond slice `frontier` are zero. */
+int kbe_unpack(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, int32_t frontier,
+               int32_t which, void* out, void* stream);
+/* Inverse: pack slices 0..frontier of a reference-layout pair (lower-stored,
+ * upper-stored) into a packed history (zeroing nothing else). */
+int kbe_pack(const void* lower_full, const void* upper_full, int32_t k_local, int32_t n_steps,
+             int32_t frontier, int64_t tri, void* hist, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KBE200_H */

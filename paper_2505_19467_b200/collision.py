@@ -1,0 +1,141 @@
+"""Collision integrals on the device (replaces kbesolve/collision.py).
+
+``collision_frontier`` runs the history-streaming ``collision_kernel``
+(K2) over the packed Sigma and G triangles and reduces its partial sums into
+the reference's ``CollisionSlice`` (collision.py:165-176).  The quadrature
+weights are closed-form in-kernel; the host functions below exist for API
+parity (collision.py:31-78).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import require_cuda, stream_ptr, to_host
+from .engine import Schedule
+from .errors import ConfigError
+from .state import _is_device_state, pack_history
+
+LIMIT_MODES = ("as-printed", "langreth")
+QUAD_KINDS = ("trapezoid", "simpson")
+DEVICE_LIMIT_MODES = ("as-printed",)
+
+
+def quadrature_weights(n: int, dt: float, kind: str = "trapezoid") -> np.ndarray:
+    """Trapezoid / Simpson (odd n: first interval trapezoid) weights (collision.py:31-61)."""
+    if n < 0:
+        raise ValueError(f"interval count must be >= 0, got {n}")
+    if n == 0:
+        return np.zeros(0)
+    if kind == "trapezoid":
+        w = np.full(n + 1, dt)
+        w[0] = w[-1] = 0.5 * dt
+        return w
+    if kind != "simpson":
+        raise ConfigError(f"quadrature kind must be 'trapezoid' or 'simpson', got {kind!r}")
+    w = np.zeros(n + 1)
+    start = 0
+    if n % 2 == 1:
+        w[0] += 0.5 * dt
+        w[1] += 0.5 * dt
+        start = 1
+        if n == 1:
+            return w
+    m = n - start
+    ws = np.full(m + 1, 2.0)
+    ws[1::2] = 4.0
+    ws[0] = ws[-1] = 1.0
+    w[start:] += ws * (dt / 3.0)
+    return w
+
+
+@dataclass(frozen=True)
+class QuadratureRule:
+    kind: str = "trapezoid"
+
+    def weights(self, n: int, dt: float) -> np.ndarray:
+        return quadrature_weights(n, dt, self.kind)
+
+
+def weight_matrix(limits, n_rows: int, dt: float, rule: QuadratureRule) -> np.ndarray:
+    """Column c holds the padded weights for interval count limits[c] (collision.py:72-78)."""
+    out = np.zeros((n_rows, len(limits)))
+    for c, lim in enumerate(limits):
+        w = rule.weights(lim, dt)
+        out[: len(w), c] = w
+    return out
+
+
+@dataclass
+class CollisionSlice:
+    """I components on the step-n frontier (collision.py:165-176)."""
+
+    lesser_row: np.ndarray
+    greater_row: np.ndarray
+    lesser_col: np.ndarray
+    greater_col: np.ndarray
+
+
+def validate_rule(kind: str, limit_mode: str) -> tuple[int, int]:
+    if limit_mode not in LIMIT_MODES:
+        raise ConfigError(f"limit_mode must be one of {LIMIT_MODES}, got {limit_mode!r}")
+    if kind not in QUAD_KINDS:
+        raise ConfigError(f"quadrature kind must be 'trapezoid' or 'simpson', got {kind!r}")
+    if limit_mode not in DEVICE_LIMIT_MODES:
+        raise ConfigError(f"limit_mode {limit_mode!r} is not implemented on the B200 device path yet")
+    return QUAD_KINDS.index(kind), LIMIT_MODES.index(limit_mode)
+
+
+def collision_frontier(state, sigma, n: int, rule: QuadratureRule = QuadratureRule(),
+                       schedule: Schedule | None = None, limit_mode: str = "as-printed",
+                       pool=None) -> CollisionSlice:
+    """Both components on all frontier pairs of step n, one K2 launch (collision.py:228-277).
+
+    Device states are read in place; reference-layout host arrays are packed
+    into temporary device histories first.
+    """
+    quad, _ = validate_rule(rule.kind, limit_mode)
+    if schedule is not None:
+        schedule.validate(state.n_k_local)
+    from .propagator import _Workspace
+    dev = require_cuda()
+    if _is_device_state(state) and isinstance(getattr(sigma, "hist", None), torch.Tensor):
+        g_hist, s_hist, n_steps = state.hist, sigma.hist, state.n_steps
+    else:
+        lesser = np.asarray(state.lesser)
+        n_steps = lesser.shape[-1] - 1
+        g_hist = pack_history(lesser, state.greater, n_steps, n)
+        s_hist = pack_history(sigma.greater, sigma.lesser, n_steps, n)
+    nk = g_hist.shape[0]
+    ws = _Workspace.for_collision(nk, n_steps, float(state.dt), quad, g_hist, s_hist, dev)
+    st = stream_ptr()
+    L = _lib.lib()
+    _lib.check(L.kbe_collision_frontier(ws.problem_ptr(), n, 0, st), "kbe_collision_frontier")
+    lr = torch.empty((nk, 2, 2, n + 1), dtype=torch.complex128, device=dev)
+    gr = torch.empty_like(lr)
+    lc = torch.empty((nk, 2, 2, n), dtype=torch.complex128, device=dev)
+    gc = torch.empty_like(lc)
+    _lib.check(L.kbe_collision_slice(ws.problem_ptr(), n, lr.data_ptr(), gr.data_ptr(), lc.data_ptr(),
+                                     gc.data_ptr(), st), "kbe_collision_slice")
+    return CollisionSlice(to_host(lr), to_host(gr), to_host(lc), to_host(gc))
+
+
+def collision_lesser(state, sigma, k: int, i: int, l: int, rule: QuadratureRule = QuadratureRule(),
+                     limit_mode: str = "as-printed") -> np.ndarray:
+    """Per-pair I<(k; t_i, t'_l) (collision.py:115-126): a row pair of frontier i
+    when i >= l, else a column pair of frontier l."""
+    if i >= l:
+        return collision_frontier(state, sigma, i, rule, None, limit_mode).lesser_row[k, :, :, l]
+    return collision_frontier(state, sigma, l, rule, None, limit_mode).lesser_col[k, :, :, i]
+
+
+def collision_greater(state, sigma, k: int, i: int, l: int, rule: QuadratureRule = QuadratureRule(),
+                      limit_mode: str = "as-printed") -> np.ndarray:
+    """Per-pair I>(k; t_i, t'_l) (collision.py:129-138)."""
+    if i >= l:
+        return collision_frontier(state, sigma, i, rule, None, limit_mode).greater_row[k, :, :, l]
+    return collision_frontier(state, sigma, l, rule, None, limit_mode).greater_col[k, :, :, i]

@@ -1,0 +1,1125 @@
+// kbe200 — B200 (sm_100a) kernels for the two-time Kadanoff–Baym step.
+//
+// Hot path of kbesolve 0.1.0 (pkg/src/kbesolve/propagator.py:316-382),
+// re-designed for one B200: a device-resident, packed, time-sliced history
+// (see include/kbe200.h), one fused launch per operator class, and
+// device-side convergence so that a step never waits on the host.
+//
+//   K1 sigma_frontier_kernel   second-Born Sigma slice (selfenergy.py:59-325)
+//   K2 collision_kernel        history-streaming I< / I> (collision.py:141-277)
+//   K3 update_kernel           predictor / corrector / residual (propagator.py:77-226)
+//   K4 finish_kernel           observables, finite check, StepReport row
+//
+// All arithmetic is FP64 / complex128.  There is no CPU fallback.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+#include <math.h>
+
+#include "../../include/kbe200.h"
+
+#define KBE_ABI_VERSION 1
+
+typedef double2 cplx;
+
+// ------------------------------------------------------------------ control
+struct kbe_ctl {
+    unsigned long long res[KBE_MAX_ITER];  // residual bits per corrector iteration
+    int nonfinite[KBE_MAX_ITER];           // frontier non-finite after iteration
+    int poisoned;                          // step that produced a non-finite frontier
+    int pad;
+    cplx hf_sum[4];                        // k-sum of rho for hf_mode="on"
+};
+
+static char g_err[512] = "";
+static void set_err(const char* what, cudaError_t e) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, e == cudaSuccess ? "bad argument" : cudaGetErrorString(e));
+}
+#define KBE_CHECK_LAUNCH(name)                                  \
+    do {                                                        \
+        cudaError_t e_ = cudaGetLastError();                    \
+        if (e_ != cudaSuccess) { set_err(name, e_); return KBE_ERR_CUDA; } \
+    } while (0)
+
+// ------------------------------------------------------------------ layout
+__host__ __device__ __forceinline__ int64_t plane_len(int s) { return (int64_t)((s + 8) >> 3) << 3; }
+__host__ __device__ __forceinline__ int64_t slice_off(int s) {
+    const int64_t q = s >> 3, r = s & 7;
+    return 64 * (q + 1) * (4 * q + r);   // 8 planes x sum_{s'<s} plane_len(s')
+}
+
+// ------------------------------------------------------------------ complex
+__device__ __forceinline__ cplx cz() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cplx cneg(cplx a) { return make_double2(-a.x, -a.y); }
+__device__ __forceinline__ cplx cconj(cplx a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ cplx cscale(cplx a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc + a*b
+__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx acc) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+// acc + a*conj(b)
+__device__ __forceinline__ cplx cfma_cb(cplx a, cplx b, cplx acc) {
+    return make_double2(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.y, b.x, fma(-a.x, b.y, acc.y)));
+}
+// acc + conj(a)*b
+__device__ __forceinline__ cplx cfma_ca(cplx a, cplx b, cplx acc) {
+    return make_double2(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
+}
+// Smith's division
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+    if (fabs(b.x) >= fabs(b.y)) {
+        const double r = b.y / b.x, den = b.x + b.y * r;
+        return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+    }
+    const double r = b.x / b.y, den = b.x * r + b.y;
+    return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+// -i*dt*z  and  +i*dt*z
+__device__ __forceinline__ cplx cmul_mi(cplx z, double dt) { return make_double2(dt * z.y, -dt * z.x); }
+__device__ __forceinline__ cplx cmul_pi(cplx z, double dt) { return make_double2(-dt * z.y, dt * z.x); }
+
+// 2x2 complex blocks, row-major: m[0]=00 m[1]=01 m[2]=10 m[3]=11
+// acc += A*B
+__device__ __forceinline__ void mm_acc(cplx* acc, const cplx* A, const cplx* B) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            cplx t = cfma(A[2 * i], B[j], acc[2 * i + j]);
+            acc[2 * i + j] = cfma(A[2 * i + 1], B[2 + j], t);
+        }
+}
+// acc += A*B^dagger : (B^dag)_{kj} = conj(B_{jk})
+__device__ __forceinline__ void mm_bdag_acc(cplx* acc, const cplx* A, const cplx* B) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            cplx t = cfma_cb(A[2 * i], B[2 * j], acc[2 * i + j]);
+            acc[2 * i + j] = cfma_cb(A[2 * i + 1], B[2 * j + 1], t);
+        }
+}
+// acc += A^dagger*B : (A^dag)_{ik} = conj(A_{ki})
+__device__ __forceinline__ void mm_adag_acc(cplx* acc, const cplx* A, const cplx* B) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            cplx t = cfma_ca(A[i], B[j], acc[2 * i + j]);
+            acc[2 * i + j] = cfma_ca(A[2 + i], B[2 + j], t);
+        }
+}
+// out = A*B
+__device__ __forceinline__ void mm(cplx* out, const cplx* A, const cplx* B) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = cz();
+    mm_acc(out, A, B);
+}
+// out = A*B^dagger
+__device__ __forceinline__ void mm_bdag(cplx* out, const cplx* A, const cplx* B) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = cz();
+    mm_bdag_acc(out, A, B);
+}
+// -(X^dagger): (-X^dag)_{jm} = -conj(X_{mj})
+__device__ __forceinline__ void neg_dag(cplx* out, const cplx* X) {
+    out[0] = cneg(cconj(X[0]));
+    out[1] = cneg(cconj(X[2]));
+    out[2] = cneg(cconj(X[1]));
+    out[3] = cneg(cconj(X[3]));
+}
+// (x - x^dagger)/2  (propagator.py:119-120)
+__device__ __forceinline__ void antiherm(cplx* out, const cplx* x) {
+    cplx t[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const cplx a = x[2 * j + m], b = cconj(x[2 * m + j]);
+            t[2 * j + m] = make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y));
+        }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = t[i];
+}
+
+// ------------------------------------------------------------------ quadrature
+// quadrature_weights(nint, dt, kind)[t]  (collision.py:31-61); 0 outside the rule.
+__device__ __forceinline__ double quad_w(int nint, int t, double dt, int quad) {
+    if (nint <= 0 || t < 0 || t > nint) return 0.0;
+    if (quad == 0) return (t == 0 || t == nint) ? 0.5 * dt : dt;
+    double w = 0.0;
+    int start = 0;
+    if (nint & 1) {
+        if (t <= 1) w = 0.5 * dt;
+        start = 1;
+        if (nint == 1) return w;
+    }
+    if (t < start) return w;
+    const int i = t - start, m = nint - start;
+    const double c = (i == 0 || i == m) ? 1.0 : ((i & 1) ? 4.0 : 2.0);
+    return __dadd_rn(w, __dmul_rn(c, dt / 3.0));
+}
+
+// ------------------------------------------------------------------ device-side convergence
+__device__ __forceinline__ bool kbe_skip(const kbe_ctl* ctl, int it, double eps) {
+    if (ctl->poisoned) return true;
+    for (int i = 0; i < it; ++i)
+        if (__longlong_as_double((long long)ctl->res[i]) <= eps) return true;
+    return false;
+}
+
+// ------------------------------------------------------------------ warp reduction
+// Sum 8 doubles over the 32 lanes with a reduce-scatter butterfly (9 shuffles);
+// lane L ends up holding the total of value index (L >> 2) & 7.
+__device__ __forceinline__ double warp_rs8(const double* v, int lane) {
+    const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+    double a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = h4 ? v[i] : v[i + 4];
+        const double keep = h4 ? v[i + 4] : v[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    double c[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = h3 ? a[i] : a[i + 2];
+        const double keep = h3 ? a[i + 2] : a[i];
+        c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const double send = h2 ? c[0] : c[1];
+    const double keep = h2 ? c[1] : c[0];
+    double d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    d += __shfl_xor_sync(0xffffffffu, d, 2);
+    d += __shfl_xor_sync(0xffffffffu, d, 1);
+    return d;
+}
+
+// =================================================================== K1: Sigma
+// Second-Born Sigma for one pair, factorised (SURVEY finding 4):
+//   P_jm(q)   = sum_k' gp_jm((k'+q-h) mod n) gr_mj(k')          (selfenergy.py:59-94)
+//   S1_jm(k)  = pref sum_q P_{j'm'}(q) gp_jm((k-q+h) mod n)      (selfenergy.py:104-136)
+//   X_jm(d)   = sum_q gr_{m'j'}((d+q) mod n) gp_{j'm}(q)
+//   S2_jm(k)  = pref sum_k' gp_{jm'}(k') X_jm((k'-k) mod n)
+//             = pref sum_{k',q} gp_{jm'}(k') gr_{m'j'}(k'+q-k) gp_{j'm}(q)   (selfenergy.py:139-203)
+// gp, gr: [k][4] complex in shared memory.  P, X: [4][nk].
+__device__ __forceinline__ int fold(int t, int n) { return t < 0 ? t + n : (t >= n ? t - n : t); }
+
+__device__ __forceinline__ cplx sig_pol(const cplx* gp, const cplx* gr, int nk, int jm, int q) {
+    const int j = jm >> 1, m = jm & 1, h = nk >> 1;
+    cplx acc = cz();
+    for (int kp = 0; kp < nk; ++kp) acc = cfma(gp[fold(kp + q - h, nk) * 4 + jm], gr[kp * 4 + m * 2 + j], acc);
+    return acc;
+}
+__device__ __forceinline__ cplx sig_x(const cplx* gp, const cplx* gr, int nk, int jm, int d) {
+    const int j = jm >> 1, m = jm & 1;
+    const int grc = (1 - m) * 2 + (1 - j), gpc = (1 - j) * 2 + m;
+    cplx acc = cz();
+    for (int q = 0; q < nk; ++q) acc = cfma(gr[fold(d + q, nk) * 4 + grc], gp[q * 4 + gpc], acc);
+    return acc;
+}
+__device__ __forceinline__ cplx sig_s1(const cplx* Pm, const cplx* gp, int nk, int jm, int k) {
+    const int jmf = 3 - jm, h = nk >> 1;   // (1-j, 1-m)
+    cplx acc = cz();
+    for (int q = 0; q < nk; ++q) acc = cfma(Pm[jmf * nk + q], gp[fold(k - q + h, nk) * 4 + jm], acc);
+    return acc;
+}
+__device__ __forceinline__ cplx sig_s2(const cplx* gp, const cplx* Xm, int nk, int jm, int k) {
+    const int j = jm >> 1, m = jm & 1;
+    const int gpc = j * 2 + (1 - m);
+    cplx acc = cz();
+    for (int kp = 0; kp < nk; ++kp) acc = cfma(gp[kp * 4 + gpc], Xm[jm * nk + fold(kp - k, nk)], acc);
+    return acc;
+}
+
+// Pairs per CTA for the fused frontier kernel.
+__host__ __device__ static int sigma_pairs_per_block(int nk) {
+    int pb = 64 / nk;
+    if (pb < 1) pb = 1;
+    if (pb > 16) pb = 16;
+    return pb;
+}
+static size_t sigma_smem_bytes(int nk, int pb) { return (size_t)32 * pb * nk * sizeof(cplx); }
+
+// K1: both components of Sigma on the step-n frontier (evaluate_sigma_batched,
+// selfenergy.py:261-325).  Pair b uses G<(t_b,t_n) and G>(t_n,t_b), read from the
+// G frontier slice n for ALL k (gathered buffer on >1 rank).
+//   lesser  (primary G<(b,n), reversed G>(n,b)) -> S<(t_b,t_n) = upper planes 4..7
+//   greater (primary G>(n,b), reversed G<(b,n)) -> S>(t_n,t_b) = lower planes 0..3
+__global__ void __launch_bounds__(256) sigma_frontier_kernel(kbe_problem P, int n, int it) {
+    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    if (kbe_skip(ctl, it, P.eps)) return;
+    extern __shared__ cplx sm[];
+    const int nk = P.n_k;
+    const int PB = sigma_pairs_per_block(nk) ;
+    const int b0 = blockIdx.x * PB;
+    const int np = min(PB, n + 1 - b0);
+    const int nloc = P.k_hi - P.k_lo;
+    cplx* V1 = sm;                       // [PB][nk][4]  G<(t_b,t_n)
+    cplx* V2 = V1 + PB * nk * 4;         // [PB][nk][4]  G>(t_n,t_b)
+    cplx* PX = V2 + PB * nk * 4;         // [PB][2 comp][2 (P,X)][4][nk]
+    cplx* OUT = PX + PB * 16 * nk;       // [PB][8][nk]
+    const int tid = threadIdx.x, nth = blockDim.x;
+
+    // frontier source: [k][8 planes][stride]
+    const cplx* src;
+    int64_t kstride, pstride;
+    if (P.front_all) {
+        src = (const cplx*)P.front_all;
+        pstride = plane_len(P.n_steps);
+        kstride = 8 * pstride;
+    } else {
+        src = (const cplx*)P.g_hist + slice_off(n);
+        pstride = plane_len(n);
+        kstride = P.tri;
+    }
+    // load + transform: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
+    for (int i = tid; i < np * nk * 8; i += nth) {
+        const int p = i % np, c = (i / np) & 7, k = i / (np * 8);
+        const int b = b0 + p;
+        const cplx v = __ldg(src + k * kstride + c * pstride + b);
+        const int cc = c & 3;
+        cplx* dst = (c < 4 ? V1 : V2) + (p * nk + k) * 4;
+        if (b < n) dst[(cc & 1) * 2 + (cc >> 1)] = cneg(cconj(v));
+        else dst[cc] = v;
+    }
+    __syncthreads();
+    // stage 1: P and X for both components; q fastest
+    for (int i = tid; i < np * 8 * nk; i += nth) {
+        const int q = i % nk, jm = (i / nk) & 3, comp = (i / (4 * nk)) & 1, p = i / (8 * nk);
+        const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
+        const cplx* gr = (comp == 0 ? V2 : V1) + p * nk * 4;
+        cplx* base = PX + (p * 2 + comp) * 8 * nk;
+        base[jm * nk + q] = sig_pol(gp, gr, nk, jm, q);
+        base[4 * nk + jm * nk + q] = sig_x(gp, gr, nk, jm, q);
+    }
+    __syncthreads();
+    // stage 2: S1 - S2 on local k
+    for (int i = tid; i < np * 8 * nloc; i += nth) {
+        const int kl = i % nloc, jm = (i / nloc) & 3, comp = (i / (4 * nloc)) & 1, p = i / (8 * nloc);
+        const int k = P.k_lo + kl, b = b0 + p;
+        const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
+        const cplx* base = PX + (p * 2 + comp) * 8 * nk;
+        const double pref = (P.u_table[b] * P.u_table[n]) / ((double)nk * (double)nk);
+        const cplx s1 = cscale(sig_s1(base, gp, nk, jm, k), pref);
+        const cplx s2 = cscale(sig_s2(gp, base + 4 * nk, nk, jm, k), pref);
+        const int plane = comp == 0 ? 4 + jm : jm;
+        OUT[(p * 8 + plane) * nk + kl] = csub(s1, s2);
+    }
+    __syncthreads();
+    cplx* dst = (cplx*)P.s_hist + slice_off(n);
+    const int64_t pl = plane_len(n);
+    for (int i = tid; i < np * 8 * nloc; i += nth) {
+        const int p = i % np, c = (i / np) & 7, kl = i / (np * 8);
+        dst[kl * P.tri + c * pl + b0 + p] = OUT[(p * 8 + c) * nk + kl];
+    }
+}
+
+// kernel-level sigma_slice API on batch-last (n_k,2,2,nb) buffers; one CTA per pair.
+__global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const cplx* gpi, const cplx* gri,
+                                                          const double* u1, const double* u2, int k_lo,
+                                                          int k_hi, const cplx* pol_in, cplx* pol_out,
+                                                          cplx* s1_out, cplx* s2_out, cplx* sig_out) {
+    extern __shared__ cplx sm[];
+    const int b = blockIdx.x;
+    cplx* gp = sm;               // [nk][4]
+    cplx* gr = gp + nk * 4;      // [nk][4]
+    cplx* Pm = gr + nk * 4;      // [4][nk]
+    cplx* Xm = Pm + nk * 4;      // [4][nk]
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (int i = tid; i < nk * 4; i += nth) {
+        gp[i] = gpi[(int64_t)i * nb + b];
+        gr[i] = gri[(int64_t)i * nb + b];
+    }
+    __syncthreads();
+    for (int i = tid; i < 4 * nk; i += nth) {
+        const int q = i % nk, jm = i / nk;
+        const cplx pv = sig_pol(gp, gr, nk, jm, q);
+        Pm[jm * nk + q] = pol_in ? pol_in[((int64_t)q * 4 + jm) * nb + b] : pv;
+        if (pol_out) pol_out[((int64_t)q * 4 + jm) * nb + b] = pv;
+        Xm[jm * nk + q] = sig_x(gp, gr, nk, jm, q);
+    }
+    __syncthreads();
+    const int nloc = k_hi - k_lo;
+    const double pref = (u1[b] * u2[b]) / ((double)nk * (double)nk);
+    for (int i = tid; i < 4 * nloc; i += nth) {
+        const int kl = i % nloc, jm = i / nloc, k = k_lo + kl;
+        const cplx s1 = cscale(sig_s1(Pm, gp, nk, jm, k), pref);
+        const cplx s2 = cscale(sig_s2(gp, Xm, nk, jm, k), pref);
+        const int64_t o = ((int64_t)kl * 4 + jm) * nb + b;
+        if (s1_out) s1_out[o] = s1;
+        if (s2_out) s2_out[o] = s2;
+        if (sig_out) sig_out[o] = csub(s1, s2);
+    }
+}
+
+// =================================================================== K2: collision
+// collision_frontier at step n (collision.py:141-277), as-printed limit, over
+// the packed histories.  Two independent triangle streams in one launch:
+//
+//  part 0 (Sigma triangle, slices 0..n) -> I<(t_n, t_l), l = 0..n:
+//    I<_row[l] = sum_tb w_tb [ G>(n,tb) S<(tb,l) - G<(n,tb) S>(tb,l) ]
+//    Each stored cell (s,b), b<=s, is read once and feeds two outputs:
+//      out[s] += w_b [A(b) SU(s,b) + B(b) SL(s,b)^dag]     (b < s)
+//      out[s] += w_s [A(s) SU(s,s) - B(s) SL(s,s)]         (b = s)
+//      out[b] -= w_s [A(s) SU(s,b)^dag + B(s) SL(s,b)]     (b < s)
+//    with A(b) = G>(t_n,t_b), B(b) = G<(t_n,t_b) (the G frontier slice).
+//  part 1 (G triangle, slices 0..n-1) -> I>(t_j, t_n), j = 0..n-1:
+//    I>_col[j] = sum_{tb<=j} w^(j)_tb [ G<(j,tb) S>(tb,n) - G>(j,tb) S<(tb,n) ]
+//             = sum w [ GU(j,tb)^dag Y(tb) - GL(j,tb) X(tb)^dag ]   (tb < j)
+//               + w [ -GU(j,j) Y(j) - GL(j,j) X(j)^dag ]            (tb = j)
+//    with X(tb) = S>(t_n,t_tb), Y(tb) = S<(t_tb,t_n) (the Sigma frontier slice).
+// I> = -I< (rows) and I< = -I> (columns) in as-printed mode (SURVEY finding 5).
+//
+// Tile = KBE_TILE_S slices x KBE_TILE_B history points; one thread per point b,
+// looping over the slices.  Row sums are warp-reduced (reduce-scatter) and
+// combined across warps in shared memory; column sums stay in registers.
+// Partials go to a workspace reduced in fixed order by the consumer (K3), so
+// results are deterministic run to run.
+#define TB KBE_TILE_B
+#define TS KBE_TILE_S
+
+__device__ __forceinline__ void load_cell(const cplx* base, int64_t pl, int b, cplx* lo, cplx* up) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) lo[c] = __ldg(base + c * pl + b);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) up[c] = __ldg(base + (4 + c) * pl + b);
+}
+
+__global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int it) {
+    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    if (kbe_skip(ctl, it, P.eps)) return;
+    const int sblk = blockIdx.x, bblk = blockIdx.y;
+    const int kl = blockIdx.z >> 1, part = blockIdx.z & 1;
+    const int smax = part == 0 ? n : n - 1;
+    const int s0 = sblk * TS;
+    if (s0 > smax) return;
+    const int s1 = min(s0 + TS - 1, smax);
+    const int bb0 = bblk * TB;
+    if (bb0 > s1) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int b = bb0 + tid;
+    const int wb0 = bb0 + warp * 32;   // first point of this warp
+    const int N1 = P.n_steps + 1;
+    const double dt = P.dt;
+
+    __shared__ cplx vec[TS][8];
+    __shared__ double rp[TB / 32][TS][8];
+
+    const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+    const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
+    const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
+    const int64_t pln = plane_len(n);
+
+    if (part == 0) {
+        // per-slice vectors w_s A(s), w_s B(s)
+        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
+            const int sl = i >> 2, c = i & 3, s = s0 + sl;
+            const double w = quad_w(n, s, dt, P.quad);
+            cplx a;
+            if (s < n) {
+                const int ct = (c & 1) * 2 + (c >> 1);
+                a = cneg(cconj(__ldg(fr + (4 + ct) * pln + s)));
+            } else {
+                a = __ldg(fr + (4 + c) * pln + s);
+            }
+            vec[sl][c] = cscale(a, w);
+            vec[sl][4 + c] = cscale(__ldg(fr + c * pln + s), w);
+        }
+        cplx Ab[4], Bb[4], col[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { Ab[c] = cz(); Bb[c] = cz(); col[c] = cz(); }
+        if (b <= s1) {
+            const double w = quad_w(n, b, dt, P.quad);
+            cplx u[4], l[4];
+            load_cell(fr, pln, b, l, u);
+            if (b < n) neg_dag(Ab, u);
+            else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) Ab[c] = u[c];
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
+        }
+        __syncthreads();
+        for (int s = s0; s <= s1; ++s) {
+            const int sl = s - s0;
+            if (wb0 > s) {   // whole warp above the diagonal
+                if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = 0.0;
+                continue;
+            }
+            cplx row[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) row[c] = cz();
+            if (b <= s) {
+                cplx SL[4], SU[4];
+                load_cell(S + slice_off(s), plane_len(s), b, SL, SU);
+                mm_acc(row, Ab, SU);
+                if (b < s) {
+                    mm_bdag_acc(row, Bb, SL);
+                    cplx As[4], Bs[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) { As[c] = vec[sl][c]; Bs[c] = vec[sl][4 + c]; }
+                    // col += As SU^dag + Bs SL
+                    mm_bdag_acc(col, As, SU);
+                    mm_acc(col, Bs, SL);
+                } else {
+                    cplx t[4];
+                    mm(t, Bb, SL);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) row[c] = csub(row[c], t[c]);
+                }
+            }
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
+            const double r = warp_rs8(v, lane);
+            if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = r;
+        }
+        __syncthreads();
+        cplx* rowP = (cplx*)P.row_part;
+        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
+            const int sl = i >> 2, c = i & 3;
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int w = 0; w < TB / 32; ++w) { re += rp[w][sl][2 * c]; im += rp[w][sl][2 * c + 1]; }
+            rowP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
+        }
+        if (b <= s1) {
+            cplx* colP = (cplx*)P.col_part;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * N1 + b) * P.nsb + sblk) * 4 + c] = cneg(col[c]);
+        }
+    } else {
+        // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
+        cplx X[4], Y[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
+        if (b <= s1) load_cell(fr, pln, b, X, Y);
+        for (int j = s0; j <= s1; ++j) {
+            const int sl = j - s0;
+            if (wb0 > j) {
+                if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = 0.0;
+                continue;
+            }
+            cplx acc[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[c] = cz();
+            if (b <= j) {
+                cplx GL[4], GU[4];
+                load_cell(G + slice_off(j), plane_len(j), b, GL, GU);
+                const double w = quad_w(j, b, dt, P.quad);
+                cplx t[4];
+                mm_bdag(t, GL, X);                 // GL X^dag
+                if (b < j) {
+                    mm_adag_acc(acc, GU, Y);       // GU^dag Y
+                } else {
+                    cplx u[4];
+                    mm(u, GU, Y);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[c] = cneg(u[c]);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] = cscale(csub(acc[c], t[c]), w);
+            }
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
+            const double r = warp_rs8(v, lane);
+            if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = r;
+        }
+        __syncthreads();
+        cplx* gcP = (cplx*)P.gc_part;
+        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
+            const int sl = i >> 2, c = i & 3;
+            double re = 0.0, im = 0.0;
+#pragma unroll
+            for (int w = 0; w < TB / 32; ++w) { re += rp[w][sl][2 * c]; im += rp[w][sl][2 * c + 1]; }
+            gcP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
+        }
+    }
+}
+
+// fixed-order reductions of the partials written by collision_kernel(nf)
+__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+    const int N1 = P.n_steps + 1;
+    const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * N1 + l) * P.nbb * 4;
+    const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * N1 + l) * P.nsb * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = cz();
+    for (int bb = 0; bb <= l / TB; ++bb)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rowP[bb * 4 + c]);
+    for (int sb = l / TS; sb <= nf / TS; ++sb)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], colP[sb * 4 + c]);
+}
+__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, cplx* out) {
+    const int N1 = P.n_steps + 1;
+    const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * N1 + j) * P.nbb * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = cz();
+    for (int bb = 0; bb <= j / TB; ++bb)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], gcP[bb * 4 + c]);
+}
+
+// kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last)
+__global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr, cplx* lc, cplx* gc) {
+    const int kl = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    cplx v[4];
+    reduce_lr(P, kl, i, n, v);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        lr[((int64_t)kl * 4 + c) * (n + 1) + i] = v[c];
+        gr[((int64_t)kl * 4 + c) * (n + 1) + i] = cneg(v[c]);
+    }
+    if (i < n) {
+        reduce_gc(P, kl, i, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            gc[((int64_t)kl * 4 + c) * n + i] = v[c];
+            lc[((int64_t)kl * 4 + c) * n + i] = cneg(v[c]);
+        }
+    }
+}
+
+// =================================================================== K3: update
+// h(k; t_{n-1/2}) (model.py:123-152) and its Cayley propagator (propagator.py:77-94).
+__device__ void build_phi(const kbe_problem& P, const kbe_ctl* ctl, int n, int k, cplx* phi) {
+    const double u = P.u_mid[n], amp = P.amp[n];
+    cplx h[4];
+    h[0] = make_double2(P.eps_v[k], 0.0);
+    h[1] = cz();
+    h[2] = cz();
+    h[3] = make_double2(P.eps_c[k] - u, 0.0);
+    if (amp != 0.0) {
+        h[1] = make_double2(amp * P.dipole_re, amp * -P.dipole_im);
+        h[2] = make_double2(amp * P.dipole_re, amp * P.dipole_im);
+    }
+    if (P.hf) {   // hartree_fock (model.py:106-120) from the k-mean of rho
+        const double inv = (double)P.n_k;
+        const cplx m00 = make_double2(ctl->hf_sum[0].x / inv, ctl->hf_sum[0].y / inv);
+        const cplx m01 = make_double2(ctl->hf_sum[1].x / inv, ctl->hf_sum[1].y / inv);
+        const cplx m10 = make_double2(ctl->hf_sum[2].x / inv, ctl->hf_sum[2].y / inv);
+        const cplx m11 = make_double2(ctl->hf_sum[3].x / inv, ctl->hf_sum[3].y / inv);
+        h[0] = cadd(h[0], make_double2(u * m11.x, 0.0));
+        h[3] = cadd(h[3], make_double2(u * m00.x, 0.0));
+        h[1] = cadd(h[1], make_double2(-u * m01.x, -u * m01.y));
+        h[2] = cadd(h[2], make_double2(-u * m10.x, -u * m10.y));
+    }
+    const double c = 0.5 * P.dt;
+    cplx a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = make_double2(-c * h[i].y, c * h[i].x);
+    const cplx m00 = make_double2(1.0 + a[0].x, a[0].y), m01 = a[1], m10 = a[2];
+    const cplx m11 = make_double2(1.0 + a[3].x, a[3].y);
+    const cplx n00 = make_double2(1.0 - a[0].x, -a[0].y), n01 = cneg(a[1]), n10 = cneg(a[2]);
+    const cplx n11 = make_double2(1.0 - a[3].x, -a[3].y);
+    const cplx det = csub(cmul(m00, m11), cmul(m01, m10));
+    phi[0] = cdiv(csub(cmul(m11, n00), cmul(m01, n10)), det);
+    phi[1] = cdiv(csub(cmul(m11, n01), cmul(m01, n11)), det);
+    phi[2] = cdiv(csub(cmul(m00, n10), cmul(m10, n00)), det);
+    phi[3] = cdiv(csub(cmul(m00, n11), cmul(m10, n01)), det);
+}
+
+__device__ __forceinline__ double absmax4(const cplx* a, const cplx* b, double r) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const double d = hypot(a[c].x - b[c].x, a[c].y - b[c].y);
+        r = (d != d || r != r) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(r, d);
+    }
+    return r;
+}
+__device__ __forceinline__ bool finite4(const cplx* a) {
+    bool ok = true;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) ok = ok && isfinite(a[c].x) && isfinite(a[c].y);
+    return ok;
+}
+
+// row(l)  = Phi (G<(n-1,l) - i dt I_row)          (propagator.py:154-155, 182-184)
+// col(j)  = (G>(j,n-1) + i dt I_col) Phi^dag      (propagator.py:156-158, 186-191)
+__device__ __forceinline__ void advance_row(const cplx* phi, const cplx* gprev, const cplx* irow, double dt, cplx* out) {
+    cplx src[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) src[c] = csub(gprev[c], cmul_pi(irow[c], dt));
+    mm(out, phi, src);
+}
+__device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, const cplx* icol, double dt, cplx* out) {
+    cplx src[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) src[c] = cadd(gprev[c], cmul_pi(icol[c], dt));
+    mm_bdag(out, src, phi);
+}
+
+__global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int phase, int it) {
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (phase == 0) {
+        if (ctl->poisoned) return;
+    } else if (kbe_skip(ctl, it, P.eps)) {
+        return;
+    }
+    const int kl = blockIdx.y, k = P.k_lo + kl;
+    __shared__ cplx phi_s[4];
+    __shared__ double red[4];
+    if (threadIdx.x == 0) build_phi(P, ctl, n, k, phi_s);
+    __syncthreads();
+    if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < KBE_MAX_ITER) {
+        ctl->res[threadIdx.x] = 0ull;
+        ctl->nonfinite[threadIdx.x] = 0;
+    }
+    cplx phi[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) phi[c] = phi_s[c];
+    const double dt = P.dt;
+    const int N1 = P.n_steps + 1;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
+    const cplx* prev = G + slice_off(n - 1);
+    const int64_t plp = plane_len(n - 1);
+    cplx* cur = G + slice_off(n);
+    const int64_t plc = plane_len(n);
+    cplx* lro = (cplx*)P.lr_old + ((int64_t)kl * N1) * 4;
+    cplx* clo = (cplx*)P.col_old + ((int64_t)kl * N1) * 4;
+    double res = 0.0;
+    bool fin = true;
+    cplx nl[4], nu[4];   // new lower (G<(n,b)) / upper (G>(b,n)) blocks
+    const bool active = b <= n;
+    if (active) {
+        if (phase == 0) {
+            if (b < n) {
+                cplx lo[4], co[4], gl[4], gu[4];
+                reduce_lr(P, kl, b, n - 1, lo);
+                if (b < n - 1) reduce_gc(P, kl, b, co);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) co[c] = cneg(lo[c]);   // greater_row[n-1] = -lesser_row[n-1]
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { lro[b * 4 + c] = lo[c]; clo[b * 4 + c] = co[c]; }
+                load_cell(prev, plp, b, gl, gu);
+                advance_row(phi, gl, lo, dt, nl);
+                advance_col(phi, gu, co, dt, nu);
+            } else {
+                cplx gl[4], gu[4], t[4], d[4];
+                load_cell(prev, plp, n - 1, gl, gu);
+                mm(t, phi, gl);
+                mm_bdag(d, t, phi);
+                antiherm(nl, d);
+                mm(t, phi, gu);
+                mm_bdag(d, t, phi);
+                antiherm(nu, d);
+            }
+        } else {
+            // corrector; b = n is the diagonal, which needs the new row/col at n-1
+            const int bb = b < n ? b : n - 1;
+            cplx lo[4], co[4], ln[4], gn[4], gl[4], gu[4], irow[4], icol[4], row[4], col[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { lo[c] = lro[bb * 4 + c]; co[c] = clo[bb * 4 + c]; }
+            reduce_lr(P, kl, bb, n, ln);
+            reduce_gc(P, kl, bb, gn);
+            load_cell(prev, plp, bb, gl, gu);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                irow[c] = cscale(cadd(lo[c], ln[c]), 0.5);
+                icol[c] = cscale(cadd(co[c], gn[c]), 0.5);
+            }
+            advance_row(phi, gl, irow, dt, row);
+            advance_col(phi, gu, icol, dt, col);
+            if (b < n) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { nl[c] = row[c]; nu[c] = col[c]; }
+            } else {
+                cplx lnn[4], ml[4], mg[4], src[4], d[4];
+                reduce_lr(P, kl, n, n, lnn);
+                neg_dag(ml, row);   // mirror of the fresh row entry (propagator.py:193)
+                neg_dag(mg, col);
+                // i_dl = (lesser_col[n-1] + lesser_row[n]) / 2, lesser_col = -greater_col
+                // i_dg = (greater_row[n-1] + greater_row[n]) / 2, greater_row = -lesser_row
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const cplx idl = cscale(cadd(cneg(gn[c]), lnn[c]), 0.5);
+                    src[c] = csub(ml[c], cmul_pi(idl, dt));
+                }
+                mm(d, phi, src);
+                antiherm(nl, d);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const cplx idg = cscale(cadd(cneg(ln[c]), cneg(lnn[c])), 0.5);
+                    src[c] = cadd(mg[c], cmul_pi(idg, dt));
+                }
+                mm_bdag(d, src, phi);
+                antiherm(nu, d);
+            }
+            cplx ol[4], ou[4];
+            load_cell(cur, plc, b, ol, ou);
+            res = absmax4(nl, ol, res);
+            res = absmax4(nu, ou, res);
+            fin = finite4(nl) && finite4(nu);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            cur[c * plc + b] = nl[c];
+            cur[(4 + c) * plc + b] = nu[c];
+        }
+        if (P.front_send) {
+            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * plane_len(P.n_steps);
+            const int64_t pm = plane_len(P.n_steps);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { fs[c * pm + b] = nl[c]; fs[(4 + c) * pm + b] = nu[c]; }
+        }
+    }
+    if (phase == 1) {
+        // block max (NaN-propagating) -> atomicMax on the bit pattern (residual >= 0)
+        for (int o = 16; o > 0; o >>= 1) {
+            const double other = __shfl_xor_sync(0xffffffffu, res, o);
+            res = (res != res || other != other) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(res, other);
+        }
+        const int nf = __syncthreads_or(!fin);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = res;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double r = red[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                r = (r != r || red[w] != red[w]) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(r, red[w]);
+            const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
+            atomicMax(&ctl->res[it], bits);
+            if (nf) atomicOr(&ctl->nonfinite[it], 1);
+        }
+    }
+}
+
+// hf_mode="on": k-sum of rho(t_{n-1}) (phase 0) or of (rho(t_{n-1}) + rho(t_n))/2 (phase 1)
+__global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(ctl, it, P.eps)) return;
+    if (threadIdx.x != 0) return;
+    const int nloc = P.k_hi - P.k_lo;
+    cplx acc[4] = {cz(), cz(), cz(), cz()};
+    for (int kl = 0; kl < nloc; ++kl) {
+        const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+        const cplx* a = G + slice_off(n - 1);
+        const int64_t pa = plane_len(n - 1);
+        for (int c = 0; c < 4; ++c) {
+            const cplx g0 = a[c * pa + (n - 1)];
+            cplx r = make_double2(g0.y, -g0.x);   // rho = -i G<
+            if (phase == 1) {
+                const cplx* bcur = G + slice_off(n);
+                const cplx g1 = bcur[c * plane_len(n) + n];
+                r = cscale(cadd(r, make_double2(g1.y, -g1.x)), 0.5);
+            }
+            acc[c] = cadd(acc[c], r);
+        }
+    }
+    for (int c = 0; c < 4; ++c) ctl->hf_sum[c] = acc[c];
+}
+
+// =================================================================== K4: finish
+__global__ void finish_kernel(kbe_problem P, int n) {
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (ctl->poisoned) return;
+    const int nloc = P.k_hi - P.k_lo;
+    __shared__ double dens[256];
+    __shared__ double drift[256];
+    for (int kl = threadIdx.x; kl < nloc; kl += blockDim.x) {
+        const cplx* c = (const cplx*)P.g_hist + (int64_t)kl * P.tri + slice_off(n);
+        const int64_t pl = plane_len(n);
+        cplx gl[4], gu[4];
+        for (int i = 0; i < 4; ++i) { gl[i] = c[i * pl + n]; gu[i] = c[(4 + i) * pl + n]; }
+        double d = 0.0;
+        for (int i = 0; i < 4; ++i) {
+            cplx t = csub(gu[i], gl[i]);
+            if (i == 0 || i == 3) t.y += 1.0;
+            d = fmax(d, hypot(t.x, t.y));
+        }
+        if (kl < 256) { dens[kl] = gl[0].y + gl[3].y; drift[kl] = d; }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double ds = 0.0, dm = 0.0;
+    for (int kl = 0; kl < nloc && kl < 256; ++kl) { ds += dens[kl]; dm = fmax(dm, drift[kl]); }
+    int iters = P.max_iter, conv = 0;
+    for (int i = 0; i < P.max_iter; ++i)
+        if (__longlong_as_double((long long)ctl->res[i]) <= P.eps) { iters = i + 1; conv = 1; break; }
+    double* r = P.reports + (int64_t)n * KBE_REPORT_W;
+    r[0] = n;
+    r[1] = iters;
+    r[2] = __longlong_as_double((long long)ctl->res[iters - 1]);
+    r[3] = conv;
+    r[4] = dm;
+    r[5] = ds;
+    r[6] = ctl->nonfinite[iters - 1];
+    r[7] = 0.0;
+    for (int i = 0; i < KBE_MAX_ITER; ++i)
+        r[8 + i] = i < iters ? __longlong_as_double((long long)ctl->res[i]) : 0.0;
+    if (ctl->nonfinite[iters - 1]) ctl->poisoned = n;
+}
+
+// =================================================================== init / pack / unpack
+__global__ void init_slice0_kernel(kbe_problem P) {
+    const int kl = blockIdx.x * blockDim.x + threadIdx.x;
+    if (kl < P.k_hi - P.k_lo) {
+        cplx* g = (cplx*)P.g_hist + (int64_t)kl * P.tri;   // slice 0: plane_len(0) = 8
+        g[0 * 8] = make_double2(0.0, 1.0);     // G<(0,0)_00 = i
+        g[7 * 8] = make_double2(0.0, -1.0);    // G>(0,0)_11 = -i
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+        memset(ctl, 0, sizeof(kbe_ctl));
+    }
+}
+
+__global__ void unpack_kernel(const cplx* hist, int64_t tri, int kloc, int N, int frontier, int which, cplx* out) {
+    const int64_t N1 = N + 1;
+    const int64_t total = (int64_t)kloc * 4 * N1 * N1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int tp = (int)(i % N1);
+        const int t = (int)((i / N1) % N1);
+        const int jm = (int)((i / (N1 * N1)) & 3);
+        const int kl = (int)(i / (N1 * N1 * 4));
+        const int j = jm >> 1, m = jm & 1;
+        const cplx* h = hist + kl * tri;
+        cplx v = cz();
+        if (t <= frontier && tp <= frontier) {
+            if (which == 0) {   // lower-stored: X(t,tp) = L(t,tp) for t >= tp
+                if (t >= tp) v = h[slice_off(t) + jm * plane_len(t) + tp];
+                else v = cneg(cconj(h[slice_off(tp) + (m * 2 + j) * plane_len(tp) + t]));
+            } else {            // upper-stored: Y(t,tp) = U(tp,t) for t <= tp
+                if (t <= tp) v = h[slice_off(tp) + (4 + jm) * plane_len(tp) + t];
+                else v = cneg(cconj(h[slice_off(t) + (4 + m * 2 + j) * plane_len(t) + tp]));
+            }
+        }
+        out[i] = v;
+    }
+}
+
+__global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int N, int frontier, int64_t tri, cplx* hist) {
+    const int64_t N1 = N + 1;
+    const int64_t per_k = slice_off(frontier + 1);
+    const int64_t total = (int64_t)kloc * per_k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kl = (int)(i / per_k);
+        const int64_t off = i % per_k;
+        // find slice s with slice_off(s) <= off < slice_off(s+1)
+        int lo = 0, hi = frontier;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (slice_off(mid) <= off) lo = mid; else hi = mid - 1;
+        }
+        const int s = lo;
+        const int64_t pl = plane_len(s);
+        const int c = (int)((off - slice_off(s)) / pl);
+        const int b = (int)((off - slice_off(s)) % pl);
+        cplx v = cz();
+        if (b <= s) {
+            if (c < 4) v = lower[(((int64_t)kl * 4 + c) * N1 + s) * N1 + b];
+            else v = upper[(((int64_t)kl * 4 + (c - 4)) * N1 + b) * N1 + s];
+        }
+        hist[kl * tri + off] = v;
+    }
+}
+
+// =================================================================== host side
+static bool g_attr_done = false;
+static int ensure_attrs() {
+    if (g_attr_done) return KBE_OK;
+    cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
+    e = cudaFuncSetAttribute(sigma_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_slice)", e); return KBE_ERR_CUDA; }
+    g_attr_done = true;
+    return KBE_OK;
+}
+
+static int check_problem(const kbe_problem* p) {
+    if (!p || p->n_k < 2 || (p->n_k & 1) || p->k_lo < 0 || p->k_hi > p->n_k || p->k_hi <= p->k_lo ||
+        p->n_steps < 1 || p->max_iter < 1 || p->max_iter > KBE_MAX_ITER || !p->g_hist || !p->s_hist || !p->ctl) {
+        set_err("kbe_problem", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    if (p->limit_mode != 0) {
+        snprintf(g_err, sizeof(g_err), "limit_mode 'langreth' is not implemented on the device path");
+        return KBE_ERR_UNSUPPORTED;
+    }
+    if (p->n_k > 256 && p->k_hi - p->k_lo > 256) {
+        snprintf(g_err, sizeof(g_err), "n_k_local > 256 not supported");
+        return KBE_ERR_UNSUPPORTED;
+    }
+    return KBE_OK;
+}
+
+extern "C" {
+
+int kbe_abi_version(void) { return KBE_ABI_VERSION; }
+int64_t kbe_plane_len(int32_t s) { return plane_len(s); }
+int64_t kbe_slice_offset(int32_t s) { return slice_off(s); }
+int64_t kbe_tri_size(int32_t n_steps) { return slice_off(n_steps + 1); }
+int64_t kbe_ctl_bytes(void) { return (int64_t)sizeof(kbe_ctl); }
+int64_t kbe_sizeof_problem(void) { return (int64_t)sizeof(kbe_problem); }
+const char* kbe_last_error(void) { return g_err; }
+
+int kbe_init_history(const kbe_problem* p, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = (size_t)(p->k_hi - p->k_lo) * p->tri * sizeof(cplx);
+    cudaError_t e = cudaMemsetAsync(p->g_hist, 0, bytes, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->s_hist, 0, bytes, st);
+    if (e != cudaSuccess) { set_err("cudaMemsetAsync(history)", e); return KBE_ERR_CUDA; }
+    const int nloc = p->k_hi - p->k_lo;
+    init_slice0_kernel<<<(nloc + 127) / 128, 128, 0, st>>>(*p);
+    KBE_CHECK_LAUNCH("init_slice0_kernel");
+    return KBE_OK;
+}
+
+int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 0 || n > p->n_steps) { set_err("kbe_sigma_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
+    if (!p->front_all && (p->k_lo != 0 || p->k_hi != p->n_k)) {
+        snprintf(g_err, sizeof(g_err), "kbe_sigma_frontier: a k-sharded rank needs the gathered frontier (front_all)");
+        return KBE_ERR_ARG;
+    }
+    if ((rc = ensure_attrs())) return rc;
+    const int pb = sigma_pairs_per_block(p->n_k);
+    const int grid = (n + 1 + pb - 1) / pb;
+    sigma_frontier_kernel<<<grid, 256, sigma_smem_bytes(p->n_k, pb), (cudaStream_t)stream>>>(*p, n, it);
+    KBE_CHECK_LAUNCH("sigma_frontier_kernel");
+    return KBE_OK;
+}
+
+int kbe_sigma_slice(int32_t n_k, int32_t nb, const void* g_primary, const void* g_reversed, const double* u1,
+                    const double* u2, int32_t k_lo, int32_t k_hi, const void* pol_in, void* pol_out, void* s1_out,
+                    void* s2_out, void* sigma_out, void* stream) {
+    if (n_k < 2 || (n_k & 1) || nb < 0 || k_lo < 0 || k_hi > n_k || k_hi < k_lo || !g_primary || !g_reversed ||
+        !u1 || !u2) {
+        set_err("kbe_sigma_slice", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    if (nb == 0) return KBE_OK;
+    int rc = ensure_attrs();
+    if (rc) return rc;
+    const size_t smem = (size_t)16 * n_k * sizeof(cplx);
+    sigma_slice_kernel<<<nb, 256, smem, (cudaStream_t)stream>>>(
+        n_k, nb, (const cplx*)g_primary, (const cplx*)g_reversed, u1, u2, k_lo, k_hi, (const cplx*)pol_in,
+        (cplx*)pol_out, (cplx*)s1_out, (cplx*)s2_out, (cplx*)sigma_out);
+    KBE_CHECK_LAUNCH("sigma_slice_kernel");
+    return KBE_OK;
+}
+
+int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
+    dim3 grid(n / TS + 1, n / TB + 1, 2 * (p->k_hi - p->k_lo));
+    collision_kernel<<<grid, TB, 0, (cudaStream_t)stream>>>(*p, n, it);
+    KBE_CHECK_LAUNCH("collision_kernel");
+    return KBE_OK;
+}
+
+int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void* greater_row, void* lesser_col,
+                        void* greater_col, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
+    collision_slice_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, (cplx*)lesser_row, (cplx*)greater_row,
+                                                                   (cplx*)lesser_col, (cplx*)greater_col);
+    KBE_CHECK_LAUNCH("collision_slice_kernel");
+    return KBE_OK;
+}
+
+int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
+    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
+    update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
+    KBE_CHECK_LAUNCH("update_kernel");
+    return KBE_OK;
+}
+
+int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    hf_mean_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
+    KBE_CHECK_LAUNCH("hf_mean_kernel");
+    return KBE_OK;
+}
+
+int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(*p, n);
+    KBE_CHECK_LAUNCH("finish_kernel");
+    return KBE_OK;
+}
+
+int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (p->front_all || p->front_send) {
+        snprintf(g_err, sizeof(g_err), "kbe_step drives one rank; multi-rank steps are sequenced by the host");
+        return KBE_ERR_ARG;
+    }
+    if (n < 1 || n > p->n_steps) { set_err("kbe_step: n", cudaSuccess); return KBE_ERR_ARG; }
+    const int nold = n - 1;
+    if (p->interacting && (rc = kbe_sigma_frontier(p, nold, 0, stream))) return rc;
+    if ((rc = kbe_collision_frontier(p, nold, 0, stream))) return rc;
+    if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
+    if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
+    for (int it = 0; it < p->max_iter; ++it) {
+        if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
+        if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
+        if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
+        if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
+    }
+    return kbe_finish_step(p, n, stream);
+}
+
+int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream) {
+    (void)use_graph;
+    for (int n = n_first; n <= n_last; ++n) {
+        int rc = kbe_step(p, n, stream);
+        if (rc) return rc;
+    }
+    return KBE_OK;
+}
+
+int kbe_unpack(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, int32_t frontier, int32_t which,
+               void* out, void* stream) {
+    if (!hist || !out || k_local < 1 || n_steps < 0 || frontier > n_steps) { set_err("kbe_unpack", cudaSuccess); return KBE_ERR_ARG; }
+    const int64_t total = (int64_t)k_local * 4 * (n_steps + 1) * (int64_t)(n_steps + 1);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    unpack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const cplx*)hist, tri, k_local, n_steps, frontier,
+                                                                 which, (cplx*)out);
+    KBE_CHECK_LAUNCH("unpack_kernel");
+    return KBE_OK;
+}
+
+int kbe_pack(const void* lower_full, const void* upper_full, int32_t k_local, int32_t n_steps, int32_t frontier,
+             int64_t tri, void* hist, void* stream) {
+    if (!lower_full || !upper_full || !hist || k_local < 1 || frontier < 0 || frontier > n_steps) {
+        set_err("kbe_pack", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    const int64_t total = (int64_t)k_local * slice_off(frontier + 1);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const cplx*)lower_full, (const cplx*)upper_full,
+                                                               k_local, n_steps, frontier, tri, (cplx*)hist);
+    KBE_CHECK_LAUNCH("pack_kernel");
+    return KBE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,366 @@
+"""Two-time stepping driver on one B200 per rank (replaces kbesolve/propagator.py).
+
+``PropagationDriver`` keeps the reference constructor, ``step()``, ``run()``,
+``state`` and ``sigma`` (propagator.py:229-392).  One step is the
+reference's Algorithm 1 (propagator.py:316-382) as a fixed launch sequence
+on one CUDA stream:
+
+    K1 Sigma(n-1) -> K2 I(n-1) -> K3 predict(n)
+    -> max_iter x [K1 Sigma(n) -> K2 I(n) -> K3 correct(n)] -> K4 finish(n)
+
+Convergence is decided on the device: K3 max-reduces the residual into a
+control block and every later launch of the step becomes a no-op once a
+residual <= eps is recorded, so the host never synchronises inside a
+step.  ``run()`` without an observer launches all steps back to back and
+reads the StepReports once at the end.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import as_device_f64, require_cuda, stream_ptr, to_host
+from .collision import validate_rule
+from .engine import Schedule, WorkerPool, shard_range
+from .errors import CapacityError, ConfigError, PoisonedStateError
+from .kgrid import KGrid
+from .model import ModelConfig, band_energies, step_tables, u_values
+from .selfenergy import SigmaHistory
+from .state import DEFAULT_MEMORY_BUDGET, TwoTimeGF, _ground_state, state_bytes
+
+
+@dataclass
+class StepConfig:
+    """Same fields, defaults and validation as propagator.py:44-62."""
+
+    dt: float
+    n_steps: int
+    eps: float = 1e-9
+    max_iter: int = 6
+    quadrature: str = "trapezoid"
+    limit_mode: str = "as-printed"
+    memory_budget: int = DEFAULT_MEMORY_BUDGET
+
+    def validate(self) -> None:
+        if self.dt <= 0:
+            raise ConfigError(f"dt must be > 0, got {self.dt}")
+        if self.n_steps < 0:
+            raise ConfigError(f"n_steps must be >= 0, got {self.n_steps}")
+        if self.eps <= 0:
+            raise ConfigError(f"eps must be > 0, got {self.eps}")
+        if self.max_iter < 1:
+            raise ConfigError(f"max_iter must be >= 1, got {self.max_iter}")
+
+
+@dataclass
+class StepReport:
+    """Per-step report (propagator.py:65-74)."""
+
+    step: int
+    iterations: int
+    residual: float
+    converged: bool
+    anticommutation_drift: float
+    density: float
+    residual_history: list = field(default_factory=list)
+    timings: dict = field(default_factory=dict)
+
+
+def cayley_propagator(h: np.ndarray, dt: float) -> np.ndarray:
+    """(1 + i dt h/2)^-1 (1 - i dt h/2) per k (propagator.py:77-94).
+
+    API parity only; the device path builds Phi inside the update kernel.
+    """
+    a = 0.5j * dt * np.asarray(h)
+    m00, m01, m10, m11 = 1.0 + a[:, 0, 0], a[:, 0, 1], a[:, 1, 0], 1.0 + a[:, 1, 1]
+    n00, n01, n10, n11 = 1.0 - a[:, 0, 0], -a[:, 0, 1], -a[:, 1, 0], 1.0 - a[:, 1, 1]
+    det = m00 * m11 - m01 * m10
+    phi = np.empty_like(a)
+    phi[:, 0, 0] = (m11 * n00 - m01 * n10) / det
+    phi[:, 0, 1] = (m11 * n01 - m01 * n11) / det
+    phi[:, 1, 0] = (m00 * n10 - m10 * n00) / det
+    phi[:, 1, 1] = (m00 * n11 - m10 * n01) / det
+    return phi
+
+
+class _Workspace:
+    """Device buffers + the ``kbe_problem`` struct handed to the C ABI.
+
+    Allocated once per driver (paper section IV-C: no allocation inside the
+    step loop); the partial-sum buffers are the K2 -> K3 hand-off.
+    """
+
+    def __init__(self, *, n_k, k_lo, k_hi, n_steps, dt, eps, max_iter, quad, limit_mode, hf,
+                 interacting, dipole, eps_v, eps_c, u_table, u_mid, amp, g_hist, s_hist, device,
+                 multi_rank=False):
+        N1 = n_steps + 1
+        kl = k_hi - k_lo
+        self.nbb = -(-N1 // _lib.TILE_B)
+        self.nsb = -(-N1 // _lib.TILE_S)
+        c128 = dict(dtype=torch.complex128, device=device)
+        self.g_hist, self.s_hist = g_hist, s_hist
+        self.row_part = torch.zeros((kl, N1, self.nbb, 4), **c128)
+        self.col_part = torch.zeros((kl, N1, self.nsb, 4), **c128)
+        self.gc_part = torch.zeros((kl, N1, self.nbb, 4), **c128)
+        self.lr_old = torch.zeros((kl, N1, 4), **c128)
+        self.col_old = torch.zeros((kl, N1, 4), **c128)
+        self.ctl = torch.zeros(int(_lib.lib().kbe_ctl_bytes()), dtype=torch.uint8, device=device)
+        self.reports = torch.zeros((N1, _lib.REPORT_W), dtype=torch.float64, device=device)
+        self.eps_v = as_device_f64(eps_v, device)
+        self.eps_c = as_device_f64(eps_c, device)
+        self.u_table = as_device_f64(u_table, device)
+        self.u_mid = as_device_f64(u_mid, device)
+        self.amp = as_device_f64(amp, device)
+        self.front_send = self.front_all = None
+        if multi_rank:
+            pm = _lib.plane_len(n_steps)
+            self.front_send = torch.zeros((kl, 8, pm), **c128)
+            self.front_all = torch.zeros((n_k, 8, pm), **c128)
+        p = _lib.KbeProblem()
+        p.n_k, p.k_lo, p.k_hi, p.n_steps = n_k, k_lo, k_hi, n_steps
+        p.quad, p.limit_mode, p.hf, p.max_iter = quad, limit_mode, int(hf), max_iter
+        p.interacting, p.nbb, p.nsb = int(interacting), self.nbb, self.nsb
+        p.dt, p.eps = float(dt), float(eps)
+        p.dipole_re, p.dipole_im = float(np.real(dipole)), float(np.imag(dipole))
+        p.tri = int(g_hist.shape[1])
+        p.g_hist, p.s_hist = g_hist.data_ptr(), s_hist.data_ptr()
+        p.eps_v, p.eps_c = self.eps_v.data_ptr(), self.eps_c.data_ptr()
+        p.u_table, p.u_mid, p.amp = self.u_table.data_ptr(), self.u_mid.data_ptr(), self.amp.data_ptr()
+        p.row_part, p.col_part, p.gc_part = (self.row_part.data_ptr(), self.col_part.data_ptr(),
+                                             self.gc_part.data_ptr())
+        p.lr_old, p.col_old = self.lr_old.data_ptr(), self.col_old.data_ptr()
+        p.front_send = self.front_send.data_ptr() if self.front_send is not None else None
+        p.front_all = self.front_all.data_ptr() if self.front_all is not None else None
+        p.ctl, p.reports = self.ctl.data_ptr(), self.reports.data_ptr()
+        self.problem = p
+
+    def problem_ptr(self) -> int:
+        return ctypes.addressof(self.problem)
+
+    # --- small workspaces for the kernel-level API ------------------------------------
+    @classmethod
+    def for_collision(cls, n_k, n_steps, dt, quad, g_hist, s_hist, device):
+        z = np.zeros(max(n_k, n_steps + 1))
+        return cls(n_k=n_k, k_lo=0, k_hi=n_k, n_steps=n_steps, dt=dt, eps=1e-9, max_iter=1, quad=quad,
+                   limit_mode=0, hf=False, interacting=True, dipole=0.0, eps_v=z[:n_k], eps_c=z[:n_k],
+                   u_table=z[: n_steps + 1], u_mid=z[: n_steps + 1], amp=z[: n_steps + 1],
+                   g_hist=g_hist, s_hist=s_hist, device=device)
+
+    @classmethod
+    def for_kernel_call(cls, grid: KGrid, state: TwoTimeGF, sigma: SigmaHistory, u_table):
+        n_k = state.n_k_local
+        z = np.zeros(max(n_k, state.n_steps + 1))
+        return cls(n_k=grid.n_k, k_lo=0, k_hi=n_k, n_steps=state.n_steps, dt=state.dt, eps=1e-9, max_iter=1,
+                   quad=0, limit_mode=0, hf=False, interacting=True, dipole=0.0, eps_v=z[:n_k], eps_c=z[:n_k],
+                   u_table=np.asarray(u_table, dtype=float)[: state.n_steps + 1],
+                   u_mid=z[: state.n_steps + 1], amp=z[: state.n_steps + 1],
+                   g_hist=state.hist, s_hist=sigma.hist, device=state.hist.device)
+
+
+def _dist_info(schedule: Schedule):
+    """(rank, world) of the k-shard group: torch.distributed when initialised."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+class PropagationDriver:
+    """Owns the device state and Sigma history and advances them (propagator.py:229-392)."""
+
+    def __init__(self, grid: KGrid, model: ModelConfig, step_cfg: StepConfig,
+                 schedule: Schedule | None = None, pool: WorkerPool | None = None):
+        model.validate()
+        step_cfg.validate()
+        self.grid = grid
+        self.model = model
+        self.cfg = step_cfg
+        self.schedule = schedule if schedule is not None else Schedule()
+        self.schedule.validate(grid.n_k)
+        self.pool = pool
+        quad, limit = validate_rule(step_cfg.quadrature, step_cfg.limit_mode)
+        if step_cfg.max_iter > _lib.MAX_ITER:
+            raise ConfigError(f"max_iter must be <= {_lib.MAX_ITER} on the device path, got {step_cfg.max_iter}")
+        capacity = max(step_cfg.n_steps, 1)
+        if 2 * state_bytes(grid.n_k, capacity) > step_cfg.memory_budget:   # propagator.py:253-259
+            raise CapacityError(
+                f"run needs {2 * state_bytes(grid.n_k, capacity)} bytes "
+                f"(n_k={grid.n_k}, n_steps={capacity}); budget is {step_cfg.memory_budget}"
+            )
+        self.capacity = capacity
+        self.u_table = u_values(model, capacity)
+        self.interactions_on = bool(np.any(self.u_table != 0.0))
+        eps_v, eps_c = band_energies(model, grid)
+        u_mid, amp = step_tables(model, self.u_table, capacity, step_cfg.dt)
+
+        self.rank, self.world = _dist_info(self.schedule)
+        self.k_lo, self.k_hi = shard_range(grid.n_k, self.rank, self.world)
+        dev = require_cuda()
+        self.device = dev
+        tri = _lib.tri_size(capacity)
+        nkl = self.k_hi - self.k_lo
+        g_hist = torch.empty((nkl, tri), dtype=torch.complex128, device=dev)
+        s_hist = torch.empty((nkl, tri), dtype=torch.complex128, device=dev)
+        self.ws = _Workspace(
+            n_k=grid.n_k, k_lo=self.k_lo, k_hi=self.k_hi, n_steps=capacity, dt=step_cfg.dt,
+            eps=step_cfg.eps, max_iter=step_cfg.max_iter, quad=quad, limit_mode=limit,
+            hf=model.hf_mode == "on", interacting=self.interactions_on, dipole=complex(model.dipole),
+            eps_v=eps_v, eps_c=eps_c, u_table=self.u_table, u_mid=u_mid, amp=amp,
+            g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1)
+        _lib.check(_lib.lib().kbe_init_history(self.ws.problem_ptr(), stream_ptr()), "kbe_init_history")
+        self.state = TwoTimeGF(nkl, self.k_lo, capacity, step_cfg.dt, g_hist, frontier=0)
+        self.sigma = SigmaHistory(s_hist, capacity)
+        self._poisoned = None
+        if self.world > 1:
+            self._gather_frontier()
+
+    # ------------------------------------------------------------------ multi-rank plumbing
+    def _gather_frontier(self) -> None:
+        """All-gather the new G slice (local k) into the all-k frontier buffer (NCCL)."""
+        import torch.distributed as dist
+        ws = self.ws
+        dist.all_gather_into_tensor(ws.front_all.view(-1), ws.front_send.view(-1))
+
+    def _allreduce_ctl(self, it: int) -> None:
+        """Global max of residual bits and non-finite flags for corrector iteration it."""
+        import torch.distributed as dist
+        res = self.ws.ctl[: 8 * _lib.MAX_ITER].view(torch.int64)
+        dist.all_reduce(res, op=dist.ReduceOp.MAX)
+        nf = self.ws.ctl[8 * _lib.MAX_ITER: 12 * _lib.MAX_ITER].view(torch.int32)
+        dist.all_reduce(nf, op=dist.ReduceOp.MAX)
+
+    def _allreduce_hf(self) -> None:
+        import torch.distributed as dist
+        off = 208   # offsetof(kbe_ctl, hf_sum): 128 res + 64 nonfinite + 8 poisoned/pad, 16-aligned
+        hf = self.ws.ctl[off: off + 64].view(torch.float64)
+        dist.all_reduce(hf, op=dist.ReduceOp.SUM)
+
+    def _launch_step(self, n: int) -> None:
+        L, P, st = _lib.lib(), self.ws.problem_ptr(), stream_ptr()
+        if self.world == 1:
+            _lib.check(L.kbe_step(P, n, st), "kbe_step")
+            return
+        # k-sharded step: same launch sequence, with one NCCL all-gather of the new
+        # G slice after every update (the Sigma input needs all k) and a MAX
+        # all-reduce of the convergence record.
+        chk = _lib.check
+        nold = n - 1
+        if self.interactions_on:
+            chk(L.kbe_sigma_frontier(P, nold, 0, st), "kbe_sigma_frontier")
+        chk(L.kbe_collision_frontier(P, nold, 0, st), "kbe_collision_frontier")
+        if self.model.hf_mode == "on":
+            chk(L.kbe_hf_mean(P, n, 0, 0, st), "kbe_hf_mean")
+            self._allreduce_hf()
+        chk(L.kbe_update(P, n, 0, 0, st), "kbe_update")
+        self._gather_frontier()
+        for it in range(self.cfg.max_iter):
+            if self.interactions_on:
+                chk(L.kbe_sigma_frontier(P, n, it, st), "kbe_sigma_frontier")
+            chk(L.kbe_collision_frontier(P, n, it, st), "kbe_collision_frontier")
+            if self.model.hf_mode == "on":
+                chk(L.kbe_hf_mean(P, n, 1, it, st), "kbe_hf_mean")
+                self._allreduce_hf()
+            chk(L.kbe_update(P, n, 1, it, st), "kbe_update")
+            self._allreduce_ctl(it)
+            self._gather_frontier()
+        chk(L.kbe_finish_step(P, n, st), "kbe_finish_step")
+
+    # ------------------------------------------------------------------ reports
+    def _reports(self, n0: int, n1: int) -> np.ndarray:
+        rows = self.ws.reports[n0: n1 + 1]
+        if self.world > 1:
+            import torch.distributed as dist
+            parts = [torch.empty_like(rows) for _ in range(self.world)]
+            dist.all_gather(parts, rows.contiguous())
+            stacked = torch.stack(parts)                   # (world, steps, W)
+            out = stacked[0].clone()
+            out[:, 4] = stacked[:, :, 4].amax(dim=0)       # drift: max over k
+            out[:, 5] = stacked[:, :, 5].sum(dim=0)        # density: sum over k
+            out[:, 6] = stacked[:, :, 6].amax(dim=0)
+            rows = out
+        return to_host(rows)
+
+    def _to_report(self, row: np.ndarray) -> StepReport:
+        it = int(row[1])
+        return StepReport(
+            step=int(row[0]), iterations=it, residual=float(row[2]), converged=bool(row[3]),
+            anticommutation_drift=float(row[4]), density=float(row[5]) / self.grid.n_k,
+            residual_history=[float(x) for x in row[8: 8 + it]], timings={},
+        )
+
+    def _precheck(self, n: int) -> None:
+        if n > self.capacity:
+            raise CapacityError(f"step {n} exceeds allocated capacity n_steps={self.capacity}")
+        if self._poisoned is not None:
+            raise PoisonedStateError(f"non-finite values on the frontier at step {self.state.frontier}")
+
+    # ------------------------------------------------------------------ API
+    def step(self) -> StepReport:
+        """One time step (propagator.py:316-382); synchronises to return its report."""
+        n = self.state.frontier + 1
+        self._precheck(n)
+        self._launch_step(n)
+        row = self._reports(n, n)[0]
+        self.state.frontier = n
+        if row[6] != 0.0:
+            self._poisoned = n
+            raise PoisonedStateError(f"non-finite values produced at step {n}")
+        return self._to_report(row)
+
+    def run(self, observer=None) -> list:
+        """Advance n_steps steps (propagator.py:384-392).
+
+        Without an observer all steps are launched back to back and the
+        reports are read once; with one, each step synchronises so the
+        observer sees the live state (as in the reference).
+        """
+        if observer is not None:
+            reports = []
+            for _ in range(self.cfg.n_steps):
+                rep = self.step()
+                reports.append(rep)
+                observer(self.state, rep)
+            return reports
+        n0 = self.state.frontier + 1
+        last = self.state.frontier + self.cfg.n_steps
+        if self.cfg.n_steps == 0:
+            return []
+        self._precheck(n0)
+        n1 = min(last, self.capacity)
+        if self.world == 1:
+            _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, 0, stream_ptr()), "kbe_run")
+        else:
+            for n in range(n0, n1 + 1):
+                self._launch_step(n)
+        rows = self._reports(n0, n1)
+        reports = []
+        for row in rows:
+            n = int(round(row[0])) if row[0] else None
+            if n is None:      # step never ran (device poisoned earlier)
+                break
+            if row[6] != 0.0:
+                self.state.frontier = n
+                self._poisoned = n
+                raise PoisonedStateError(f"non-finite values produced at step {n}")
+            reports.append(self._to_report(row))
+        self.state.frontier = n1
+        if last > self.capacity:
+            raise CapacityError(f"step {self.capacity + 1} exceeds allocated capacity n_steps={self.capacity}")
+        return reports
+
+    def synchronize(self) -> None:
+        torch.cuda.current_stream().synchronize()
+
+
+def run(grid: KGrid, model: ModelConfig, step_cfg: StepConfig, schedule: Schedule | None = None,
+        pool: WorkerPool | None = None, observer=None):
+    """Propagate a fresh state for step_cfg.n_steps steps (propagator.py:395-406)."""
+    driver = PropagationDriver(grid, model, step_cfg, schedule, pool)
+    reports = driver.run(observer=observer)
+    return driver.state, reports

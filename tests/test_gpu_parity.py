@@ -1,0 +1,212 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle and the reference goldens.
+
+Tolerances: kernel level <= 1e-12 relative (SURVEY §8(c) protocol 1),
+trajectories <= 1e-10 relative (BASELINE.json north_star), densities 1e-12 abs.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel_err
+from oracle import kbe_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_19467_b200 as kb  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+# ------------------------------------------------------------------ Sigma (kernel level)
+@pytest.mark.parametrize("n_k", [2, 4, 8, 16, 32, 64])
+def test_sigma_slice_matches_reference_golden(n_k):
+    g = load_golden("sigma.npz")
+    grid = kb.build_kgrid(n_k)
+    gl, gg = g[f"gl_{n_k}"], g[f"gg_{n_k}"]
+    u1, u2 = g[f"u1_{n_k}"], float(g[f"u2_{n_k}"])
+    pol = kb.polarizability(gl, gg, grid)
+    assert rel_err(pol, g[f"pol_{n_k}"]) <= 1e-12
+    assert rel_err(kb.sigma_first(g[f"pol_{n_k}"], gl, u1, u2, grid), g[f"s1_{n_k}"]) <= 1e-12
+    assert rel_err(kb.sigma_second(gl, gg, u1, u2, grid), g[f"s2_{n_k}"]) <= 1e-12
+    assert rel_err(kb.sigma_slice(gl, gg, u1, u2, grid), g[f"sigma_{n_k}"]) <= 1e-12
+    shard = kb.sigma_slice(gl, gg, u1, u2, grid, (n_k // 2, n_k))
+    assert rel_err(shard, g[f"sigma_shard_{n_k}"]) <= 1e-12
+
+
+@pytest.mark.parametrize("n_k", [2, 16, 128])
+def test_sigma_slice_matches_oracle_random(n_k):
+    rng = np.random.default_rng(n_k)
+    shape = (n_k, 2, 2, 7)
+    gl = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    gg = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    u1 = rng.uniform(0.5, 1.5, 7)
+    grid = kb.build_kgrid(n_k)
+    got = kb.sigma_slice(gl, gg, u1, 0.8, grid)
+    want = O.sigma_slice(gl, gg, u1, 0.8)
+    assert rel_err(got, want) <= 1e-12
+    # 3-D input squeezes back (selfenergy.py:55-56)
+    one = kb.sigma_slice(gl[..., 0], gg[..., 0], 1.0, 1.0, grid)
+    assert one.shape == (n_k, 2, 2)
+
+
+def test_sigma_batched_matches_reference_golden():
+    g = load_golden("sigma_batched.npz")
+    GL, GG, u = g["GL"], g["GG"], g["u"]
+    n_k, cap = GL.shape[0], GL.shape[-1] - 1
+    grid = kb.build_kgrid(n_k)
+    for n in (0, 3, 6):
+        state = kb.TwoTimeGF.from_arrays(GL, GG, dt=0.05, frontier=cap)
+        sigma = kb.init_sigma_history(n_k, cap)
+        kb.evaluate_sigma_batched(state, sigma, n, grid, u)
+        assert rel_err(sigma.lesser, g[f"SL_{n}"]) <= 1e-12
+        assert rel_err(sigma.greater, g[f"SG_{n}"]) <= 1e-12
+
+
+# ------------------------------------------------------------------ collision (kernel level)
+class _Arrays:
+    def __init__(self, lesser, greater, dt=0.05):
+        self.lesser, self.greater, self.dt = lesser, greater, dt
+        self.n_k_local = lesser.shape[0]
+
+
+@pytest.mark.parametrize("kind", ["trapezoid", "simpson"])
+@pytest.mark.parametrize("n", [0, 1, 2, 5, 8])
+def test_collision_matches_reference_golden(kind, n):
+    g = load_golden("collision.npz")
+    state = _Arrays(g["GL"], g["GG"], float(g["dt"]))
+    sigma = _Arrays(g["SL"], g["SG"])
+    c = kb.collision_frontier(state, sigma, n, kb.QuadratureRule(kind))
+    tag = f"{kind}_as-printed_{n}"
+    for name, got in (("lr", c.lesser_row), ("gr", c.greater_row), ("lc", c.lesser_col), ("gc", c.greater_col)):
+        want = g[f"{name}_{tag}"]
+        assert got.shape == want.shape
+        if want.size:
+            assert rel_err(got, want) <= 1e-12, name
+
+
+def test_collision_pair_matches_reference_golden():
+    g = load_golden("collision.npz")
+    state = _Arrays(g["GL"], g["GG"], float(g["dt"]))
+    sigma = _Arrays(g["SL"], g["SG"])
+    assert rel_err(kb.collision_lesser(state, sigma, 1, 5, 2), g["pair_lesser_k1_i5_l2"]) <= 1e-12
+    assert rel_err(kb.collision_greater(state, sigma, 2, 3, 6), g["pair_greater_k2_i3_l6"]) <= 1e-12
+
+
+def _random_sym_history(n_k, cap, seed):
+    GL, GG = O.random_mirrored_state(n_k, cap, cap, seed)
+    rng = np.random.default_rng(seed + 1)
+    shape = GL.shape
+    SL = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    SG = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    for n in range(1, cap + 1):
+        SL[:, :, :, n, :n] = -np.conj(np.swapaxes(SL[:, :, :, :n, n], 1, 2))
+        SG[:, :, :, :n, n] = -np.conj(np.swapaxes(SG[:, :, :, n, :n], 1, 2))
+    return GL, GG, SL, SG
+
+
+@pytest.mark.parametrize("kind", ["trapezoid", "simpson"])
+@pytest.mark.parametrize("n", [63, 64, 127, 128, 129, 200, 301])
+def test_collision_multi_tile_matches_oracle(kind, n):
+    """Tile edges of K2 (64 slices x 128 points) against the oracle."""
+    n_k = 2
+    GL, GG, SL, SG = _random_sym_history(n_k, n, seed=n)
+    c = kb.collision_frontier(_Arrays(GL, GG), _Arrays(SL, SG), n, kb.QuadratureRule(kind))
+    want = O.collision_frontier(GL, GG, SL, SG, n, 0.05, kind)
+    assert rel_err(c.lesser_row, want.lesser_row) <= 1e-12
+    assert rel_err(c.greater_row, want.greater_row) <= 1e-12
+    assert rel_err(c.lesser_col, want.lesser_col) <= 1e-12
+    assert rel_err(c.greater_col, want.greater_col) <= 1e-12
+
+
+def test_langreth_is_rejected_loudly():
+    g = load_golden("collision.npz")
+    with pytest.raises(kb.ConfigError):
+        kb.collision_frontier(_Arrays(g["GL"], g["GG"]), _Arrays(g["SL"], g["SG"]), 3, limit_mode="langreth")
+
+
+# ------------------------------------------------------------------ trajectories (reference goldens)
+def _driver_from_fixture(g):
+    model = kb.ModelConfig(
+        band_gap=float(g["band_gap"]), hopping=float(g["hopping"]),
+        u_protocol=(float(g["u_protocol"]) if g["u_protocol"].ndim == 0 else g["u_protocol"]),
+        pulse_intensity=float(g["pulse_intensity"]), pulse_center=float(g["pulse_center"]),
+        dipole=complex(g["dipole"]), hf_mode=str(g["hf_mode"]),
+        eps_c_table=g["eps_c_table"] if "eps_c_table" in g else None,
+        eps_v_table=g["eps_v_table"] if "eps_v_table" in g else None,
+    )
+    cfg = kb.StepConfig(dt=float(g["dt"]), n_steps=int(g["n_steps"]), eps=float(g["eps"]),
+                        max_iter=int(g["max_iter"]), quadrature=str(g["quadrature"]),
+                        limit_mode=str(g["limit_mode"]), memory_budget=1 << 40)
+    return kb.PropagationDriver(kb.build_kgrid(int(g["n_k"])), model, cfg)
+
+
+TRAJ = ["traj_nk4_full.npz", "traj_hf.npz", "traj_simpson.npz", "traj_nk64_synth.npz",
+        "traj_dimer.npz", "traj_free.npz", "traj_nk16.npz"]
+
+
+@pytest.mark.parametrize("name", TRAJ)
+def test_trajectory_matches_reference_golden(name):
+    g = load_golden(name)
+    drv = _driver_from_fixture(g)
+    reps = drv.run()
+    N = int(g["n_steps"])
+    GL, GG = drv.state.lesser, drv.state.greater
+    idx = np.arange(N + 1)
+    assert rel_err(GL[:, :, :, idx, idx], g["diag_lesser"]) <= 1e-10
+    assert rel_err(GG[:, :, :, idx, idx], g["diag_greater"]) <= 1e-10
+    assert rel_err(GL[:, :, :, N, :], g["final_row_lesser"]) <= 1e-10
+    assert rel_err(GG[:, :, :, :, N], g["final_col_greater"]) <= 1e-10
+    np.testing.assert_allclose([r.density for r in reps], g["density"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose([r.anticommutation_drift for r in reps], g["drift"], rtol=0, atol=1e-10)
+    flips = np.sum(np.array([r.iterations for r in reps]) != g["iterations"])
+    assert flips <= max(1, N // 50)
+    if "GL" in g:
+        assert rel_err(GL, g["GL"]) <= 1e-10
+        assert rel_err(GG, g["GG"]) <= 1e-10
+        assert rel_err(drv.sigma.lesser, g["SL"]) <= 1e-10
+        assert rel_err(drv.sigma.greater, g["SG"]) <= 1e-10
+    if "rows_lesser" in g:
+        for s, row, col in zip(g["row_steps"], g["rows_lesser"], g["cols_greater"]):
+            assert rel_err(GL[:, :, :, s, :], row) <= 1e-10
+            assert rel_err(GG[:, :, :, :, s], col) <= 1e-10
+
+
+def test_step_by_step_equals_batched_run():
+    g = load_golden("traj_nk4_full.npz")
+    a = _driver_from_fixture(g)
+    ra = a.run()
+    b = _driver_from_fixture(g)
+    rb = [b.step() for _ in range(int(g["n_steps"]))]
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    assert torch.equal(a.state.hist, b.state.hist)       # bitwise determinism
+    assert torch.equal(a.sigma.hist, b.sigma.hist)
+
+
+def test_poisoned_state_raises():
+    model = kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.1)
+    drv = kb.PropagationDriver(kb.build_kgrid(4), model, kb.StepConfig(dt=0.02, n_steps=10))
+    drv.step()
+    drv.state.hist[0, kb_slice_entry(1)] = complex(float("nan"), 0.0)
+    with pytest.raises(kb.PoisonedStateError):
+        drv.run()
+
+
+def kb_slice_entry(s):
+    from paper_2505_19467_b200 import _lib
+    return _lib.slice_offset(s)
+
+
+def test_capacity_errors():
+    model = kb.ModelConfig(u_protocol=1.0)
+    with pytest.raises(kb.CapacityError):
+        kb.PropagationDriver(kb.build_kgrid(16), model, kb.StepConfig(dt=0.02, n_steps=1000))
+    drv = kb.PropagationDriver(kb.build_kgrid(2), model, kb.StepConfig(dt=0.02, n_steps=2))
+    drv.run()
+    with pytest.raises(kb.CapacityError):
+        drv.step()
