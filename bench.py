@@ -1,8 +1,9 @@
 """KBE time-steps/sec on B200 (BASELINE.json metric) -- see DESIGN.md §Measurement.
 
 Workload (BASELINE.json configs[1]): 1D Hubbard chain n_k=16, second-Born,
-1000 time steps, dt=0.02, U=1, delta pulse I=0.2 at t=0.5, reference model
-defaults otherwise.  One bench "step" = one whole propagation
+1000 time steps, dt=0.02, U=0.5, delta pulse I=0.2 at t=0.5, reference model
+defaults otherwise.  U=0.5 rather than SURVEY's U=1: with U=1
+the reference's own as-printed scheme diverges at step 667.  One bench "step" = one whole propagation
 of the 1000 time steps from the ground state; value = time steps per second
 of whole-job throughput (all ranks), inputs already on the device.
 
@@ -33,7 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KBE time-steps/sec (whole propagation)"
-CFG = dict(n_k=16, n_steps=1000, dt=0.02, u=1.0, pulse_intensity=0.2, pulse_center=0.5)
+CFG = dict(n_k=16, n_steps=1000, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5)
 WORKLOAD = "cfg2: 1D Hubbard chain n_k=16, second-Born, 1000 time steps"
 
 
@@ -94,7 +95,7 @@ def cpu_baseline(iterations_per_step=None, budget_s=25.0):
     GPU run's iteration counts (1 + it_n evaluations at step n)."""
     from oracle import kbe_oracle as O
     n_k, N, dt = CFG["n_k"], CFG["n_steps"], CFG["dt"]
-    ns = [40, 80, 120, 160]
+    ns = [100, 200, 300]
     cap = max(ns)
     drv = O.OracleDriver(n_k, O.Model(u_protocol=1.0), dt, cap)
     GL, GG = O.random_mirrored_state(n_k, cap, cap, seed=3)
@@ -283,6 +284,8 @@ def run_ours(args):
         _barrier(world)
     secs = _max_over_ranks(t0.elapsed_time(t1) * 1e-3, world)
     reps = drv._reports(1, N)
+    if np.any(reps[:, 6] != 0) or np.any(reps[:, 0] == 0):
+        raise RuntimeError("propagation poisoned or incomplete inside the timed region")
     iters = reps[:, 1].astype(int)
     dens = reps[:, 5] / CFG["n_k"]
     value = args.steps * N / secs

@@ -393,6 +393,54 @@ __device__ __forceinline__ void load_cell(const cplx* base, int64_t pl, int b, c
     for (int c = 0; c < 4; ++c) up[c] = __ldg(base + (4 + c) * pl + b);
 }
 
+// ---- TMA bulk copies + mbarriers (sm_90+ async proxy), one pipeline per warp
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define KBE_STAGES 4
+#define KBE_WARPS (TB / 32)
+// dynamic shared memory of collision_kernel
+struct CollSmem {
+    cplx buf[KBE_WARPS][KBE_STAGES][8][32];   // per-warp ring of slice cells (8 planes x 32 points)
+    cplx vec[TS][8];                          // per-slice frontier vectors (Sigma part)
+    double rp[KBE_WARPS][TS][8];              // per-warp row partials
+    uint64_t bar[KBE_WARPS][KBE_STAGES];
+};
+
+// Issue the 8 plane copies of slice s, points [wb0, wb0+32) clipped to the plane.
+__device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar) {
+    const int64_t pl = plane_len(s);
+    const int cnt = (int)min((int64_t)32, pl - wb0);
+    const uint32_t bytes = (uint32_t)cnt * 16u;
+    mbar_expect_tx(bar, 8u * bytes);
+    const cplx* base = hist + slice_off(s) + wb0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar);
+}
+
 __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int it) {
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
@@ -404,22 +452,36 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
     const int s1 = min(s0 + TS - 1, smax);
     const int bb0 = bblk * TB;
     if (bb0 > s1) return;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b = bb0 + tid;
     const int wb0 = bb0 + warp * 32;   // first point of this warp
     const int N1 = P.n_steps + 1;
     const double dt = P.dt;
 
-    __shared__ cplx vec[TS][8];
-    __shared__ double rp[TB / 32][TS][8];
-
     const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
     const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
     const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
+    const cplx* hist = part == 0 ? S : G;                   // streamed triangle
     const int64_t pln = plane_len(n);
 
+    // this warp's slices: those with at least one point b <= s
+    const int sf = max(s0, wb0);
+    const int m = s1 - sf + 1;   // may be <= 0
+    uint64_t* bars = sm.bar[warp];
+    if (lane == 0) {
+        for (int i = 0; i < KBE_STAGES; ++i) mbar_init(&bars[i], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (int i = 0; i < KBE_STAGES && i < m; ++i) issue_slice(hist, sf + i, wb0, sm.buf[warp][i], &bars[i]);
+    for (int s = s0; s < sf && s <= s1; ++s)
+        if ((lane & 3) == 0) sm.rp[warp][s - s0][lane >> 2] = 0.0;
+
     if (part == 0) {
-        // per-slice vectors w_s A(s), w_s B(s)
+        // per-slice vectors w_s A(s), w_s B(s);  A(s) = G>(t_n,t_s), B(s) = G<(t_n,t_s)
         for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
             const int sl = i >> 2, c = i & 3, s = s0 + sl;
             const double w = quad_w(n, s, dt, P.quad);
@@ -430,8 +492,8 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
             } else {
                 a = __ldg(fr + (4 + c) * pln + s);
             }
-            vec[sl][c] = cscale(a, w);
-            vec[sl][4 + c] = cscale(__ldg(fr + c * pln + s), w);
+            sm.vec[sl][c] = cscale(a, w);
+            sm.vec[sl][4 + c] = cscale(__ldg(fr + c * pln + s), w);
         }
         cplx Ab[4], Bb[4], col[4];
 #pragma unroll
@@ -449,26 +511,26 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
             for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
         }
         __syncthreads();
-        for (int s = s0; s <= s1; ++s) {
-            const int sl = s - s0;
-            if (wb0 > s) {   // whole warp above the diagonal
-                if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = 0.0;
-                continue;
-            }
+        for (int i = 0; i < m; ++i) {
+            const int s = sf + i, sl = s - s0, st = i % KBE_STAGES;
+            mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
+            cplx SL[4], SU[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[warp][st][c][lane]; SU[c] = sm.buf[warp][st][4 + c][lane]; }
+            __syncwarp();
+            if (lane == 0 && i + KBE_STAGES < m)
+                issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[warp][st], &bars[st]);
             cplx row[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) row[c] = cz();
             if (b <= s) {
-                cplx SL[4], SU[4];
-                load_cell(S + slice_off(s), plane_len(s), b, SL, SU);
                 mm_acc(row, Ab, SU);
                 if (b < s) {
                     mm_bdag_acc(row, Bb, SL);
                     cplx As[4], Bs[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) { As[c] = vec[sl][c]; Bs[c] = vec[sl][4 + c]; }
-                    // col += As SU^dag + Bs SL
-                    mm_bdag_acc(col, As, SU);
+                    for (int c = 0; c < 4; ++c) { As[c] = sm.vec[sl][c]; Bs[c] = sm.vec[sl][4 + c]; }
+                    mm_bdag_acc(col, As, SU);   // col += As SU^dag + Bs SL
                     mm_acc(col, Bs, SL);
                 } else {
                     cplx t[4];
@@ -481,7 +543,7 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
             const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = r;
+            if ((lane & 3) == 0) sm.rp[warp][sl][lane >> 2] = r;
         }
         __syncthreads();
         cplx* rowP = (cplx*)P.row_part;
@@ -489,7 +551,7 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
             const int sl = i >> 2, c = i & 3;
             double re = 0.0, im = 0.0;
 #pragma unroll
-            for (int w = 0; w < TB / 32; ++w) { re += rp[w][sl][2 * c]; im += rp[w][sl][2 * c + 1]; }
+            for (int w = 0; w < KBE_WARPS; ++w) { re += sm.rp[w][sl][2 * c]; im += sm.rp[w][sl][2 * c + 1]; }
             rowP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
         }
         if (b <= s1) {
@@ -503,18 +565,19 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
 #pragma unroll
         for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
         if (b <= s1) load_cell(fr, pln, b, X, Y);
-        for (int j = s0; j <= s1; ++j) {
-            const int sl = j - s0;
-            if (wb0 > j) {
-                if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = 0.0;
-                continue;
-            }
+        for (int i = 0; i < m; ++i) {
+            const int j = sf + i, sl = j - s0, st = i % KBE_STAGES;
+            mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
+            cplx GL[4], GU[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[warp][st][c][lane]; GU[c] = sm.buf[warp][st][4 + c][lane]; }
+            __syncwarp();
+            if (lane == 0 && i + KBE_STAGES < m)
+                issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[warp][st], &bars[st]);
             cplx acc[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[c] = cz();
             if (b <= j) {
-                cplx GL[4], GU[4];
-                load_cell(G + slice_off(j), plane_len(j), b, GL, GU);
                 const double w = quad_w(j, b, dt, P.quad);
                 cplx t[4];
                 mm_bdag(t, GL, X);                 // GL X^dag
@@ -533,7 +596,7 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
             const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) rp[warp][sl][lane >> 2] = r;
+            if ((lane & 3) == 0) sm.rp[warp][sl][lane >> 2] = r;
         }
         __syncthreads();
         cplx* gcP = (cplx*)P.gc_part;
@@ -541,7 +604,7 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
             const int sl = i >> 2, c = i & 3;
             double re = 0.0, im = 0.0;
 #pragma unroll
-            for (int w = 0; w < TB / 32; ++w) { re += rp[w][sl][2 * c]; im += rp[w][sl][2 * c + 1]; }
+            for (int w = 0; w < KBE_WARPS; ++w) { re += sm.rp[w][sl][2 * c]; im += sm.rp[w][sl][2 * c + 1]; }
             gcP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
         }
     }
@@ -935,6 +998,8 @@ static int ensure_attrs() {
     if (g_attr_done) return KBE_OK;
     cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
+    e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
+    if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(sigma_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_slice)", e); return KBE_ERR_CUDA; }
     g_attr_done = true;
@@ -1021,8 +1086,9 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
+    if ((rc = ensure_attrs())) return rc;
     dim3 grid(n / TS + 1, n / TB + 1, 2 * (p->k_hi - p->k_lo));
-    collision_kernel<<<grid, TB, 0, (cudaStream_t)stream>>>(*p, n, it);
+    collision_kernel<<<grid, TB, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
     KBE_CHECK_LAUNCH("collision_kernel");
     return KBE_OK;
 }

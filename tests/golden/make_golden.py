@@ -232,7 +232,42 @@ def trajectory_fixtures():
     )
 
 
+def cfg2_full_fixture():
+    """The bench workload itself (BASELINE configs[1]) run by the REAL reference:
+    n_k=16, 1000 steps, U=0.5 (U=1 diverges at step 667 in the reference's own
+    scheme), pulse 0.2 at t=0.5.  k-sharded over 6 worker threads
+    (bitwise identical to 1 shard, SURVEY probe P5).  Stores the final row/column,
+    the equal-time diagonals and the per-step observables."""
+    n_k, N = 16, 1000
+    grid = kb.build_kgrid(n_k)
+    model = kb.ModelConfig(u_protocol=0.5, pulse_intensity=0.2, pulse_center=0.5)
+    cfg = kb.StepConfig(dt=0.02, n_steps=N, memory_budget=8 * 1024**3)
+    workers = int(os.environ.get("KBE_GOLDEN_WORKERS", "6"))
+    shards = 8 if workers >= 8 else (4 if workers >= 4 else 1)
+    pool = kb.WorkerPool(workers)
+    t0 = time.time()
+    drv = kb.PropagationDriver(grid, model, cfg, kb.Schedule(n_shards=shards, workers=workers), pool)
+    reps = []
+    for n in range(1, N + 1):
+        reps.append(drv.step())
+        if n % 50 == 0:
+            print(f"  cfg2 step {n} {time.time() - t0:.0f}s", flush=True)
+    st = drv.state
+    idx = np.arange(N + 1)
+    _save("traj_cfg2_full.npz",
+          n_k=np.array(n_k), n_steps=np.array(N), dt=np.array(0.02), u=np.array(0.5),
+          pulse_intensity=np.array(0.2), pulse_center=np.array(0.5),
+          iterations=np.array([r.iterations for r in reps]),
+          drift=np.array([r.anticommutation_drift for r in reps]),
+          density=np.array([r.density for r in reps]),
+          diag_lesser=st.lesser[:, :, :, idx, idx],
+          final_row_lesser=st.lesser[:, :, :, N, :],
+          final_col_greater=st.greater[:, :, :, :, N],
+          ref_seconds=np.array(time.time() - t0))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["sigma", "collision", "sigma_batched", "trajectory"]
     for w in which:
         globals()[f"{w}_fixture" if w != "trajectory" else "trajectory_fixtures"]()
+
