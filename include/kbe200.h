@@ -42,8 +42,8 @@ extern "C" {
 #define KBE_ERR_UNSUPPORTED 3
 
 #define KBE_MAX_ITER 16      /* StepConfig.max_iter ceiling on the device path */
-#define KBE_TILE_B 128       /* collision tile: history points per CTA        */
-#define KBE_TILE_S 64        /* collision tile: time slices per CTA           */
+#define KBE_TILE_B 32        /* collision warp-task: history points            */
+#define KBE_TILE_S 32        /* collision warp-task: time slices               */
 #define KBE_REPORT_W 24      /* doubles per StepReport row (8 + KBE_MAX_ITER)  */
 
 /* Report row layout (doubles):

@@ -16,8 +16,8 @@ LIB_PATH = os.environ.get("KBE200_LIB", os.path.join(_HERE, "libkbe200.so"))
 
 KBE_OK, KBE_ERR_ARG, KBE_ERR_CUDA, KBE_ERR_UNSUPPORTED = 0, 1, 2, 3
 MAX_ITER = 16
-TILE_B = 128
-TILE_S = 64
+TILE_B = 32
+TILE_S = 32
 REPORT_W = 24
 ABI_VERSION = 1
 

@@ -413,6 +413,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -420,14 +422,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  : "memory");
 }
 
-#define KBE_STAGES 4
-#define KBE_WARPS (TB / 32)
-// dynamic shared memory of collision_kernel
+#define KBE_STAGES 3
+// dynamic shared memory of one collision warp-task
 struct CollSmem {
-    cplx buf[KBE_WARPS][KBE_STAGES][8][32];   // per-warp ring of slice cells (8 planes x 32 points)
-    cplx vec[TS][8];                          // per-slice frontier vectors (Sigma part)
-    double rp[KBE_WARPS][TS][8];              // per-warp row partials
-    uint64_t bar[KBE_WARPS][KBE_STAGES];
+    cplx buf[KBE_STAGES][8][32];   // ring of slice cells: 8 planes x 32 points
+    cplx vec[TS][8];               // per-slice frontier vectors (Sigma part)
+    uint64_t bar[KBE_STAGES];
 };
 
 // Issue the 8 plane copies of slice s, points [wb0, wb0+32) clipped to the plane.
@@ -441,22 +441,34 @@ __device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cp
     for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar);
 }
 
-__global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int it) {
+// triangular index t -> (sc, bc) with 0 <= bc <= sc
+__device__ __forceinline__ void tri_decode(int t, int& sc, int& bc) {
+    int s = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((s + 1) * (s + 2) / 2 <= t) ++s;
+    while (s * (s + 1) / 2 > t) --s;
+    sc = s;
+    bc = t - s * (s + 1) / 2;
+}
+
+// One warp = one task of 32 history points x 32 slices; no CTA-level barriers,
+// a 3-stage TMA bulk-copy ring per warp keeps ~8 KB per warp in flight.
+__global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
-    const int sblk = blockIdx.x, bblk = blockIdx.y;
-    const int kl = blockIdx.z >> 1, part = blockIdx.z & 1;
+    const int part = blockIdx.y, kl = blockIdx.z;
     const int smax = part == 0 ? n : n - 1;
-    const int s0 = sblk * TS;
-    if (s0 > smax) return;
-    const int s1 = min(s0 + TS - 1, smax);
-    const int bb0 = bblk * TB;
-    if (bb0 > s1) return;
+    if (smax < 0) return;
+    const int T = smax / TS + 1;
+    if ((int)blockIdx.x >= T * (T + 1) / 2) return;
+    int sc, bc;
+    tri_decode(blockIdx.x, sc, bc);
+    const int s0 = sc * TS, s1 = min(s0 + TS - 1, smax);
+    const int wb0 = bc * TB;            // wb0 <= s0: every slice has lane 0 valid
+    const int m = s1 - s0 + 1;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int b = bb0 + tid;
-    const int wb0 = bb0 + warp * 32;   // first point of this warp
+    const int lane = threadIdx.x;
+    const int b = wb0 + lane;
     const int N1 = P.n_steps + 1;
     const double dt = P.dt;
 
@@ -465,35 +477,30 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
     const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
     const cplx* hist = part == 0 ? S : G;                   // streamed triangle
     const int64_t pln = plane_len(n);
-
-    // this warp's slices: those with at least one point b <= s
-    const int sf = max(s0, wb0);
-    const int m = s1 - sf + 1;   // may be <= 0
-    uint64_t* bars = sm.bar[warp];
+    uint64_t* bars = sm.bar;
     if (lane == 0) {
         for (int i = 0; i < KBE_STAGES; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
     }
     __syncwarp();
     if (lane == 0)
-        for (int i = 0; i < KBE_STAGES && i < m; ++i) issue_slice(hist, sf + i, wb0, sm.buf[warp][i], &bars[i]);
-    for (int s = s0; s < sf && s <= s1; ++s)
-        if ((lane & 3) == 0) sm.rp[warp][s - s0][lane >> 2] = 0.0;
+        for (int i = 0; i < KBE_STAGES && i < m; ++i) issue_slice(hist, s0 + i, wb0, sm.buf[i], &bars[i]);
+    double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
 
     if (part == 0) {
         // per-slice vectors w_s A(s), w_s B(s);  A(s) = G>(t_n,t_s), B(s) = G<(t_n,t_s)
-        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
-            const int sl = i >> 2, c = i & 3, s = s0 + sl;
+        if (lane < m) {
+            const int s = s0 + lane;
             const double w = quad_w(n, s, dt, P.quad);
-            cplx a;
-            if (s < n) {
-                const int ct = (c & 1) * 2 + (c >> 1);
-                a = cneg(cconj(__ldg(fr + (4 + ct) * pln + s)));
-            } else {
-                a = __ldg(fr + (4 + c) * pln + s);
+            cplx u[4], l[4], a[4];
+            load_cell(fr, pln, s, l, u);
+            if (s < n) neg_dag(a, u);
+            else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a[c] = u[c];
             }
-            sm.vec[sl][c] = cscale(a, w);
-            sm.vec[sl][4 + c] = cscale(__ldg(fr + c * pln + s), w);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = cscale(a[c], w); sm.vec[lane][4 + c] = cscale(l[c], w); }
         }
         cplx Ab[4], Bb[4], col[4];
 #pragma unroll
@@ -510,16 +517,13 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
 #pragma unroll
             for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
         }
-        __syncthreads();
+        __syncwarp();
         for (int i = 0; i < m; ++i) {
-            const int s = sf + i, sl = s - s0, st = i % KBE_STAGES;
+            const int s = s0 + i, st = i % KBE_STAGES;
             mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
             cplx SL[4], SU[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[warp][st][c][lane]; SU[c] = sm.buf[warp][st][4 + c][lane]; }
-            __syncwarp();
-            if (lane == 0 && i + KBE_STAGES < m)
-                issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[warp][st], &bars[st]);
+            for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[st][c][lane]; SU[c] = sm.buf[st][4 + c][lane]; }
             cplx row[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) row[c] = cz();
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
                     mm_bdag_acc(row, Bb, SL);
                     cplx As[4], Bs[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) { As[c] = sm.vec[sl][c]; Bs[c] = sm.vec[sl][4 + c]; }
+                    for (int c = 0; c < 4; ++c) { As[c] = sm.vec[i][c]; Bs[c] = sm.vec[i][4 + c]; }
                     mm_bdag_acc(col, As, SU);   // col += As SU^dag + Bs SL
                     mm_acc(col, Bs, SL);
                 } else {
@@ -542,22 +546,17 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
             double v[8];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
-            const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) sm.rp[warp][sl][lane >> 2] = r;
-        }
-        __syncthreads();
-        cplx* rowP = (cplx*)P.row_part;
-        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
-            const int sl = i >> 2, c = i & 3;
-            double re = 0.0, im = 0.0;
-#pragma unroll
-            for (int w = 0; w < KBE_WARPS; ++w) { re += sm.rp[w][sl][2 * c]; im += sm.rp[w][sl][2 * c + 1]; }
-            rowP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
+            const double r = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
+            if ((lane & 3) == 0) outP[(((int64_t)kl * N1 + s) * P.nbb + bc) * 8 + (lane >> 2)] = r;
+            // refill stage st only after every lane has consumed it (WAR across proxies)
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
         }
         if (b <= s1) {
             cplx* colP = (cplx*)P.col_part;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * N1 + b) * P.nsb + sblk) * 4 + c] = cneg(col[c]);
+            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * N1 + b) * P.nsb + sc) * 4 + c] = cneg(col[c]);
         }
     } else {
         // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
@@ -566,14 +565,11 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
         for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
         if (b <= s1) load_cell(fr, pln, b, X, Y);
         for (int i = 0; i < m; ++i) {
-            const int j = sf + i, sl = j - s0, st = i % KBE_STAGES;
+            const int j = s0 + i, st = i % KBE_STAGES;
             mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
             cplx GL[4], GU[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[warp][st][c][lane]; GU[c] = sm.buf[warp][st][4 + c][lane]; }
-            __syncwarp();
-            if (lane == 0 && i + KBE_STAGES < m)
-                issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[warp][st], &bars[st]);
+            for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[st][c][lane]; GU[c] = sm.buf[st][4 + c][lane]; }
             cplx acc[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[c] = cz();
@@ -596,62 +592,62 @@ __global__ void __launch_bounds__(TB) collision_kernel(kbe_problem P, int n, int
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
             const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) sm.rp[warp][sl][lane >> 2] = r;
-        }
-        __syncthreads();
-        cplx* gcP = (cplx*)P.gc_part;
-        for (int i = tid; i < (s1 - s0 + 1) * 4; i += TB) {
-            const int sl = i >> 2, c = i & 3;
-            double re = 0.0, im = 0.0;
-#pragma unroll
-            for (int w = 0; w < KBE_WARPS; ++w) { re += sm.rp[w][sl][2 * c]; im += sm.rp[w][sl][2 * c + 1]; }
-            gcP[(((int64_t)kl * N1 + s0 + sl) * P.nbb + bblk) * 4 + c] = make_double2(re, im);
+            if ((lane & 3) == 0) outP[(((int64_t)kl * N1 + j) * P.nbb + bc) * 8 + (lane >> 2)] = r;
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
         }
     }
 }
 
-// fixed-order reductions of the partials written by collision_kernel(nf)
-__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+// Warp-cooperative fixed-order sum of partial blocks pa[0..na) + pb[0..nb) (4 complex
+// each); every lane returns the total.
+__device__ __forceinline__ void warp_sum_partials(const cplx* pa, int na, const cplx* pb, int nb, int lane,
+                                                  cplx* out) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = 0.0;
+    for (int i = lane; i < na; i += 32)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const cplx x = pa[i * 4 + c]; v[2 * c] += x.x; v[2 * c + 1] += x.y; }
+    for (int i = lane; i < nb; i += 32)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { const cplx x = pb[i * 4 + c]; v[2 * c] += x.x; v[2 * c + 1] += x.y; }
+    const double r = warp_rs8(v, lane);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        out[c] = make_double2(__shfl_sync(0xffffffffu, r, 8 * c), __shfl_sync(0xffffffffu, r, 8 * c + 4));
+}
+// I<(t_nf, t_l) from the partials of collision_kernel(nf)
+__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, int lane, cplx* out) {
     const int N1 = P.n_steps + 1;
     const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * N1 + l) * P.nbb * 4;
-    const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * N1 + l) * P.nsb * 4;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) out[c] = cz();
-    for (int bb = 0; bb <= l / TB; ++bb)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rowP[bb * 4 + c]);
-    for (int sb = l / TS; sb <= nf / TS; ++sb)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], colP[sb * 4 + c]);
+    const cplx* colP = (const cplx*)P.col_part + (((int64_t)kl * N1 + l) * P.nsb + l / TS) * 4;
+    warp_sum_partials(rowP, l / TB + 1, colP, nf / TS - l / TS + 1, lane, out);
 }
-__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, cplx* out) {
+// I>(t_j, t_nf) from the partials of collision_kernel(nf), j < nf
+__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, int lane, cplx* out) {
     const int N1 = P.n_steps + 1;
     const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * N1 + j) * P.nbb * 4;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) out[c] = cz();
-    for (int bb = 0; bb <= j / TB; ++bb)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], gcP[bb * 4 + c]);
+    warp_sum_partials(gcP, j / TB + 1, nullptr, 0, lane, out);
 }
 
-// kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last)
+// kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last); warp per point
 __global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr, cplx* lc, cplx* gc) {
-    const int kl = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int kl = blockIdx.y, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i > n) return;
     cplx v[4];
-    reduce_lr(P, kl, i, n, v);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        lr[((int64_t)kl * 4 + c) * (n + 1) + i] = v[c];
-        gr[((int64_t)kl * 4 + c) * (n + 1) + i] = cneg(v[c]);
+    reduce_lr(P, kl, i, n, lane, v);
+    if (lane < 4) {
+        lr[((int64_t)kl * 4 + lane) * (n + 1) + i] = v[lane];
+        gr[((int64_t)kl * 4 + lane) * (n + 1) + i] = cneg(v[lane]);
     }
     if (i < n) {
-        reduce_gc(P, kl, i, v);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            gc[((int64_t)kl * 4 + c) * n + i] = v[c];
-            lc[((int64_t)kl * 4 + c) * n + i] = cneg(v[c]);
+        reduce_gc(P, kl, i, lane, v);
+        if (lane < 4) {
+            gc[((int64_t)kl * 4 + lane) * n + i] = v[lane];
+            lc[((int64_t)kl * 4 + lane) * n + i] = cneg(v[lane]);
         }
     }
 }
@@ -725,6 +721,9 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
     mm_bdag(out, src, phi);
 }
 
+// One warp per frontier point b (b = n is the equal-time diagonal).  The warp
+// reduces the K2 partials cooperatively; every lane then holds identical
+// values, lanes 0..7 write one plane each.
 __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int phase, int it) {
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
@@ -733,20 +732,18 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         return;
     }
     const int kl = blockIdx.y, k = P.k_lo + kl;
-    __shared__ cplx phi_s[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ double red[4];
-    if (threadIdx.x == 0) build_phi(P, ctl, n, k, phi_s);
-    __syncthreads();
+    __shared__ int redf[4];
     if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < KBE_MAX_ITER) {
         ctl->res[threadIdx.x] = 0ull;
         ctl->nonfinite[threadIdx.x] = 0;
     }
     cplx phi[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) phi[c] = phi_s[c];
+    build_phi(P, ctl, n, k, phi);
     const double dt = P.dt;
     const int N1 = P.n_steps + 1;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.x * 4 + warp;
     cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
     const cplx* prev = G + slice_off(n - 1);
     const int64_t plp = plane_len(n - 1);
@@ -756,20 +753,18 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     cplx* clo = (cplx*)P.col_old + ((int64_t)kl * N1) * 4;
     double res = 0.0;
     bool fin = true;
-    cplx nl[4], nu[4];   // new lower (G<(n,b)) / upper (G>(b,n)) blocks
-    const bool active = b <= n;
-    if (active) {
+    if (b <= n) {
+        cplx nl[4], nu[4];   // new lower (G<(n,b)) / upper (G>(b,n)) blocks
         if (phase == 0) {
             if (b < n) {
                 cplx lo[4], co[4], gl[4], gu[4];
-                reduce_lr(P, kl, b, n - 1, lo);
-                if (b < n - 1) reduce_gc(P, kl, b, co);
+                reduce_lr(P, kl, b, n - 1, lane, lo);
+                if (b < n - 1) reduce_gc(P, kl, b, lane, co);
                 else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) co[c] = cneg(lo[c]);   // greater_row[n-1] = -lesser_row[n-1]
                 }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { lro[b * 4 + c] = lo[c]; clo[b * 4 + c] = co[c]; }
+                if (lane < 4) { lro[b * 4 + lane] = lo[lane]; clo[b * 4 + lane] = co[lane]; }
                 load_cell(prev, plp, b, gl, gu);
                 advance_row(phi, gl, lo, dt, nl);
                 advance_col(phi, gu, co, dt, nu);
@@ -789,8 +784,8 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             cplx lo[4], co[4], ln[4], gn[4], gl[4], gu[4], irow[4], icol[4], row[4], col[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { lo[c] = lro[bb * 4 + c]; co[c] = clo[bb * 4 + c]; }
-            reduce_lr(P, kl, bb, n, ln);
-            reduce_gc(P, kl, bb, gn);
+            reduce_lr(P, kl, bb, n, lane, ln);
+            reduce_gc(P, kl, bb, lane, gn);
             load_cell(prev, plp, bb, gl, gu);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -804,7 +799,7 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
                 for (int c = 0; c < 4; ++c) { nl[c] = row[c]; nu[c] = col[c]; }
             } else {
                 cplx lnn[4], ml[4], mg[4], src[4], d[4];
-                reduce_lr(P, kl, n, n, lnn);
+                reduce_lr(P, kl, n, n, lane, lnn);
                 neg_dag(ml, row);   // mirror of the fresh row entry (propagator.py:193)
                 neg_dag(mg, col);
                 // i_dl = (lesser_col[n-1] + lesser_row[n]) / 2, lesser_col = -greater_col
@@ -830,31 +825,26 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             res = absmax4(nu, ou, res);
             fin = finite4(nl) && finite4(nu);
         }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            cur[c * plc + b] = nl[c];
-            cur[(4 + c) * plc + b] = nu[c];
-        }
-        if (P.front_send) {
-            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * plane_len(P.n_steps);
-            const int64_t pm = plane_len(P.n_steps);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { fs[c * pm + b] = nl[c]; fs[(4 + c) * pm + b] = nu[c]; }
+        __syncwarp();
+        if (lane < 8) {
+            const cplx v = lane < 4 ? nl[lane & 3] : nu[lane & 3];
+            cur[lane * plc + b] = v;
+            if (P.front_send) {
+                const int64_t pm = plane_len(P.n_steps);
+                ((cplx*)P.front_send)[(int64_t)kl * 8 * pm + lane * pm + b] = v;
+            }
         }
     }
     if (phase == 1) {
-        // block max (NaN-propagating) -> atomicMax on the bit pattern (residual >= 0)
-        for (int o = 16; o > 0; o >>= 1) {
-            const double other = __shfl_xor_sync(0xffffffffu, res, o);
-            res = (res != res || other != other) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(res, other);
-        }
-        const int nf = __syncthreads_or(!fin);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = res;
+        if (lane == 0) { red[warp] = res; redf[warp] = fin ? 0 : 1; }
         __syncthreads();
         if (threadIdx.x == 0) {
             double r = red[0];
-            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            int nf = redf[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
                 r = (r != r || red[w] != red[w]) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(r, red[w]);
+                nf |= redf[w];
+            }
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
             atomicMax(&ctl->res[it], bits);
             if (nf) atomicOr(&ctl->nonfinite[it], 1);
@@ -1087,8 +1077,9 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
-    dim3 grid(n / TS + 1, n / TB + 1, 2 * (p->k_hi - p->k_lo));
-    collision_kernel<<<grid, TB, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
+    const int T = n / TS + 1;
+    dim3 grid(T * (T + 1) / 2, 2, p->k_hi - p->k_lo);
+    collision_kernel<<<grid, 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
     KBE_CHECK_LAUNCH("collision_kernel");
     return KBE_OK;
 }
@@ -1097,7 +1088,7 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
                         void* greater_col, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
+    dim3 grid((n + 1 + 3) / 4, p->k_hi - p->k_lo);
     collision_slice_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, (cplx*)lesser_row, (cplx*)greater_row,
                                                                    (cplx*)lesser_col, (cplx*)greater_col);
     KBE_CHECK_LAUNCH("collision_slice_kernel");
@@ -1108,7 +1099,7 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
+    dim3 grid((n + 1 + 3) / 4, p->k_hi - p->k_lo);
     update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
     KBE_CHECK_LAUNCH("update_kernel");
     return KBE_OK;

@@ -111,9 +111,9 @@ def _random_sym_history(n_k, cap, seed):
 
 
 @pytest.mark.parametrize("kind", ["trapezoid", "simpson"])
-@pytest.mark.parametrize("n", [63, 64, 127, 128, 129, 200, 301])
+@pytest.mark.parametrize("n", [31, 32, 33, 63, 64, 65, 127, 128, 200, 301])
 def test_collision_multi_tile_matches_oracle(kind, n):
-    """Tile edges of K2 (64 slices x 128 points) against the oracle."""
+    """Task edges of K2 (32 slices x 32 points per warp) against the oracle."""
     n_k = 2
     GL, GG, SL, SG = _random_sym_history(n_k, n, seed=n)
     c = kb.collision_frontier(_Arrays(GL, GG), _Arrays(SL, SG), n, kb.QuadratureRule(kind))
