@@ -85,6 +85,7 @@ typedef struct kbe_problem {
     void* front_all;      /* NULL (1 rank) or [n_k][8][plane_len(N)] (allgathered)  */
     void* ctl;            /* kbe_ctl_bytes() of device control state               */
     double* reports;      /* [N+1][KBE_REPORT_W]                                   */
+    void* phi;            /* [N+1][k_local][4] complex: Cayley propagator per step */
 } kbe_problem;
 
 /* ---- layout helpers (host-callable, no device work) ---------------------- */
@@ -143,6 +144,11 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
  * rho(t_{n-1}), phase 1 uses (rho(t_{n-1}) + rho(t_n))/2.  Local k sum;
  * the caller all-reduces across ranks before dividing (kbe_hf_finalize). */
 int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
+
+/* Phi(t_{n-1/2}) for local k into p->phi[n] after the host has all-reduced the
+ * hf k-sum across ranks (hf_mode="on" with k-shards; one rank does this inside
+ * kbe_hf_mean).  The table for hf_mode="off" is built by kbe_init_history. */
+int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream);
 
 /* End of step n: observables_at / anticommutation_drift (state.py:125-137),
  * _frontier_finite (propagator.py:223-226), StepReport row into reports[n].

@@ -41,7 +41,7 @@ class KbeProblem(ctypes.Structure):
         ("row_part", _p), ("col_part", _p), ("gc_part", _p),
         ("lr_old", _p), ("col_old", _p),
         ("front_send", _p), ("front_all", _p),
-        ("ctl", _p), ("reports", _p),
+        ("ctl", _p), ("reports", _p), ("phi", _p),
     ]
 
 
@@ -61,6 +61,7 @@ SIGNATURES = {
     "kbe_collision_slice": (ctypes.c_int, [_p, _i32, _p, _p, _p, _p, _p]),
     "kbe_update": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_hf_mean": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
+    "kbe_build_phi": (ctypes.c_int, [_p, _i32, _i32, _p]),
     "kbe_finish_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_run": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),

@@ -209,63 +209,65 @@ __device__ __forceinline__ double warp_rs8(const double* v, int lane) {
 //   X_jm(d)   = sum_q gr_{m'j'}((d+q) mod n) gp_{j'm}(q)
 //   S2_jm(k)  = pref sum_k' gp_{jm'}(k') X_jm((k'-k) mod n)
 //             = pref sum_{k',q} gp_{jm'}(k') gr_{m'j'}(k'+q-k) gp_{j'm}(q)   (selfenergy.py:139-203)
-// gp, gr: [k][4] complex in shared memory.  P, X: [4][nk].
+// Shared-memory operands are planar: gp[jm * nk + k]; P and X likewise [jm][q].
 __device__ __forceinline__ int fold(int t, int n) { return t < 0 ? t + n : (t >= n ? t - n : t); }
 
 __device__ __forceinline__ cplx sig_pol(const cplx* gp, const cplx* gr, int nk, int jm, int q) {
     const int j = jm >> 1, m = jm & 1, h = nk >> 1;
+    const cplx* a = gp + jm * nk;
+    const cplx* c = gr + (m * 2 + j) * nk;
     cplx acc = cz();
-    for (int kp = 0; kp < nk; ++kp) acc = cfma(gp[fold(kp + q - h, nk) * 4 + jm], gr[kp * 4 + m * 2 + j], acc);
+    for (int kp = 0; kp < nk; ++kp) acc = cfma(a[fold(kp + q - h, nk)], c[kp], acc);
     return acc;
 }
 __device__ __forceinline__ cplx sig_x(const cplx* gp, const cplx* gr, int nk, int jm, int d) {
     const int j = jm >> 1, m = jm & 1;
-    const int grc = (1 - m) * 2 + (1 - j), gpc = (1 - j) * 2 + m;
+    const cplx* a = gr + ((1 - m) * 2 + (1 - j)) * nk;
+    const cplx* c = gp + ((1 - j) * 2 + m) * nk;
     cplx acc = cz();
-    for (int q = 0; q < nk; ++q) acc = cfma(gr[fold(d + q, nk) * 4 + grc], gp[q * 4 + gpc], acc);
+    for (int q = 0; q < nk; ++q) acc = cfma(a[fold(d + q, nk)], c[q], acc);
     return acc;
 }
 __device__ __forceinline__ cplx sig_s1(const cplx* Pm, const cplx* gp, int nk, int jm, int k) {
-    const int jmf = 3 - jm, h = nk >> 1;   // (1-j, 1-m)
+    const int h = nk >> 1;
+    const cplx* a = Pm + (3 - jm) * nk;   // P_{(1-j)(1-m)}
+    const cplx* c = gp + jm * nk;
     cplx acc = cz();
-    for (int q = 0; q < nk; ++q) acc = cfma(Pm[jmf * nk + q], gp[fold(k - q + h, nk) * 4 + jm], acc);
+    for (int q = 0; q < nk; ++q) acc = cfma(a[q], c[fold(k - q + h, nk)], acc);
     return acc;
 }
 __device__ __forceinline__ cplx sig_s2(const cplx* gp, const cplx* Xm, int nk, int jm, int k) {
     const int j = jm >> 1, m = jm & 1;
-    const int gpc = j * 2 + (1 - m);
+    const cplx* a = gp + (j * 2 + (1 - m)) * nk;
+    const cplx* c = Xm + jm * nk;
     cplx acc = cz();
-    for (int kp = 0; kp < nk; ++kp) acc = cfma(gp[kp * 4 + gpc], Xm[jm * nk + fold(kp - k, nk)], acc);
+    for (int kp = 0; kp < nk; ++kp) acc = cfma(a[kp], c[fold(kp - k, nk)], acc);
     return acc;
 }
 
-// Pairs per CTA for the fused frontier kernel.
-__host__ __device__ static int sigma_pairs_per_block(int nk) {
-    int pb = 64 / nk;
-    if (pb < 1) pb = 1;
-    if (pb > 16) pb = 16;
-    return pb;
-}
-static size_t sigma_smem_bytes(int nk, int pb) { return (size_t)32 * pb * nk * sizeof(cplx); }
+// K1 launch shape: 8*n_k threads per pair (one per (component, jm, q)); small n_k
+// packs several pairs per 128-thread CTA.
+__host__ __device__ __forceinline__ int sigma_threads(int nk) { return 8 * nk < 128 ? 128 : 8 * nk; }
+__host__ __device__ __forceinline__ int sigma_pairs_per_block(int nk) { return sigma_threads(nk) / (8 * nk); }
+static size_t sigma_smem_bytes(int nk, int pb) { return (size_t)24 * pb * nk * sizeof(cplx); }
 
 // K1: both components of Sigma on the step-n frontier (evaluate_sigma_batched,
 // selfenergy.py:261-325).  Pair b uses G<(t_b,t_n) and G>(t_n,t_b), read from the
 // G frontier slice n for ALL k (gathered buffer on >1 rank).
 //   lesser  (primary G<(b,n), reversed G>(n,b)) -> S<(t_b,t_n) = upper planes 4..7
 //   greater (primary G>(n,b), reversed G<(b,n)) -> S>(t_n,t_b) = lower planes 0..3
-__global__ void __launch_bounds__(256) sigma_frontier_kernel(kbe_problem P, int n, int it) {
+__global__ void __launch_bounds__(1024) sigma_frontier_kernel(kbe_problem P, int n, int it) {
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
     extern __shared__ cplx sm[];
     const int nk = P.n_k;
-    const int PB = sigma_pairs_per_block(nk) ;
+    const int PB = sigma_pairs_per_block(nk);
     const int b0 = blockIdx.x * PB;
     const int np = min(PB, n + 1 - b0);
     const int nloc = P.k_hi - P.k_lo;
-    cplx* V1 = sm;                       // [PB][nk][4]  G<(t_b,t_n)
-    cplx* V2 = V1 + PB * nk * 4;         // [PB][nk][4]  G>(t_n,t_b)
+    cplx* V1 = sm;                       // [PB][4][nk]  G<(t_b,t_n)
+    cplx* V2 = V1 + PB * nk * 4;         // [PB][4][nk]  G>(t_n,t_b)
     cplx* PX = V2 + PB * nk * 4;         // [PB][2 comp][2 (P,X)][4][nk]
-    cplx* OUT = PX + PB * 16 * nk;       // [PB][8][nk]
     const int tid = threadIdx.x, nth = blockDim.x;
 
     // frontier source: [k][8 planes][stride]
@@ -286,39 +288,33 @@ __global__ void __launch_bounds__(256) sigma_frontier_kernel(kbe_problem P, int 
         const int b = b0 + p;
         const cplx v = __ldg(src + k * kstride + c * pstride + b);
         const int cc = c & 3;
-        cplx* dst = (c < 4 ? V1 : V2) + (p * nk + k) * 4;
-        if (b < n) dst[(cc & 1) * 2 + (cc >> 1)] = cneg(cconj(v));
-        else dst[cc] = v;
+        cplx* dst = (c < 4 ? V1 : V2) + p * nk * 4;
+        if (b < n) dst[((cc & 1) * 2 + (cc >> 1)) * nk + k] = cneg(cconj(v));
+        else dst[cc * nk + k] = v;
     }
     __syncthreads();
-    // stage 1: P and X for both components; q fastest
-    for (int i = tid; i < np * 8 * nk; i += nth) {
-        const int q = i % nk, jm = (i / nk) & 3, comp = (i / (4 * nk)) & 1, p = i / (8 * nk);
-        const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
-        const cplx* gr = (comp == 0 ? V2 : V1) + p * nk * 4;
-        cplx* base = PX + (p * 2 + comp) * 8 * nk;
+    const int per = 8 * nk;
+    const int p = tid / per, r = tid % per;
+    const int comp = r / (4 * nk), jm = (r / nk) & 3, q = r % nk;
+    const bool act = p < np;
+    const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
+    const cplx* gr = (comp == 0 ? V2 : V1) + p * nk * 4;
+    cplx* base = PX + (p * 2 + comp) * 8 * nk;
+    // stage 1: P and X, one (component, jm, q) per thread
+    if (act) {
         base[jm * nk + q] = sig_pol(gp, gr, nk, jm, q);
         base[4 * nk + jm * nk + q] = sig_x(gp, gr, nk, jm, q);
     }
     __syncthreads();
-    // stage 2: S1 - S2 on local k
-    for (int i = tid; i < np * 8 * nloc; i += nth) {
-        const int kl = i % nloc, jm = (i / nloc) & 3, comp = (i / (4 * nloc)) & 1, p = i / (8 * nloc);
-        const int k = P.k_lo + kl, b = b0 + p;
-        const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
-        const cplx* base = PX + (p * 2 + comp) * 8 * nk;
+    // stage 2: S1 - S2 on local k (q indexes the local k)
+    if (act && q < nloc) {
+        const int k = P.k_lo + q, b = b0 + p;
         const double pref = (P.u_table[b] * P.u_table[n]) / ((double)nk * (double)nk);
         const cplx s1 = cscale(sig_s1(base, gp, nk, jm, k), pref);
         const cplx s2 = cscale(sig_s2(gp, base + 4 * nk, nk, jm, k), pref);
         const int plane = comp == 0 ? 4 + jm : jm;
-        OUT[(p * 8 + plane) * nk + kl] = csub(s1, s2);
-    }
-    __syncthreads();
-    cplx* dst = (cplx*)P.s_hist + slice_off(n);
-    const int64_t pl = plane_len(n);
-    for (int i = tid; i < np * 8 * nloc; i += nth) {
-        const int p = i % np, c = (i / np) & 7, kl = i / (np * 8);
-        dst[kl * P.tri + c * pl + b0 + p] = OUT[(p * 8 + c) * nk + kl];
+        cplx* dst = (cplx*)P.s_hist + slice_off(n);
+        dst[(int64_t)q * P.tri + plane * plane_len(n) + b] = csub(s1, s2);
     }
 }
 
@@ -329,14 +325,15 @@ __global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const 
                                                           cplx* s1_out, cplx* s2_out, cplx* sig_out) {
     extern __shared__ cplx sm[];
     const int b = blockIdx.x;
-    cplx* gp = sm;               // [nk][4]
-    cplx* gr = gp + nk * 4;      // [nk][4]
+    cplx* gp = sm;               // [4][nk]
+    cplx* gr = gp + nk * 4;      // [4][nk]
     cplx* Pm = gr + nk * 4;      // [4][nk]
     cplx* Xm = Pm + nk * 4;      // [4][nk]
     const int tid = threadIdx.x, nth = blockDim.x;
     for (int i = tid; i < nk * 4; i += nth) {
-        gp[i] = gpi[(int64_t)i * nb + b];
-        gr[i] = gri[(int64_t)i * nb + b];
+        const int k = i >> 2, jm = i & 3;
+        gp[jm * nk + k] = gpi[(int64_t)i * nb + b];
+        gr[jm * nk + k] = gri[(int64_t)i * nb + b];
     }
     __syncthreads();
     for (int i = tid; i < 4 * nk; i += nth) {
@@ -547,7 +544,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
             const double r = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
-            if ((lane & 3) == 0) outP[(((int64_t)kl * N1 + s) * P.nbb + bc) * 8 + (lane >> 2)] = r;
+            if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)] = r;
             // refill stage st only after every lane has consumed it (WAR across proxies)
             fence_proxy_async();
             __syncwarp();
@@ -556,7 +553,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         if (b <= s1) {
             cplx* colP = (cplx*)P.col_part;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * N1 + b) * P.nsb + sc) * 4 + c] = cneg(col[c]);
+            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c] = cneg(col[c]);
         }
     } else {
         // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
@@ -592,7 +589,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #pragma unroll
             for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
             const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) outP[(((int64_t)kl * N1 + j) * P.nbb + bc) * 8 + (lane >> 2)] = r;
+            if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)] = r;
             fence_proxy_async();
             __syncwarp();
             if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
@@ -600,54 +597,58 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
     }
 }
 
-// Warp-cooperative fixed-order sum of partial blocks pa[0..na) + pb[0..nb) (4 complex
-// each); every lane returns the total.
-__device__ __forceinline__ void warp_sum_partials(const cplx* pa, int na, const cplx* pb, int nb, int lane,
-                                                  cplx* out) {
-    double v[8];
+// Fixed-order reductions of the partials written by collision_kernel(nf).
+// Partial planes are [k][chunk][point][4 complex], so consecutive points (threads)
+// read consecutive 64-byte blocks for every chunk.
+// I<(t_nf, t_l) = sum over b-chunks of the row sums + sum over s-chunks of the column sums
+__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+    const int64_t N1 = P.n_steps + 1;
+    const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + l) * 4;
+    const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + l) * 4;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = 0.0;
-    for (int i = lane; i < na; i += 32)
+    for (int c = 0; c < 4; ++c) out[c] = cz();
+    const int nr = l / TB;
+#pragma unroll 4
+    for (int bc = 0; bc <= nr; ++bc)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { const cplx x = pa[i * 4 + c]; v[2 * c] += x.x; v[2 * c + 1] += x.y; }
-    for (int i = lane; i < nb; i += 32)
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rowP[bc * N1 * 4 + c]);
+    const int s_hi = nf / TS;
+#pragma unroll 4
+    for (int sc = l / TS; sc <= s_hi; ++sc)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) { const cplx x = pb[i * 4 + c]; v[2 * c] += x.x; v[2 * c + 1] += x.y; }
-    const double r = warp_rs8(v, lane);
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-        out[c] = make_double2(__shfl_sync(0xffffffffu, r, 8 * c), __shfl_sync(0xffffffffu, r, 8 * c + 4));
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], colP[sc * N1 * 4 + c]);
 }
-// I<(t_nf, t_l) from the partials of collision_kernel(nf)
-__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, int lane, cplx* out) {
-    const int N1 = P.n_steps + 1;
-    const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * N1 + l) * P.nbb * 4;
-    const cplx* colP = (const cplx*)P.col_part + (((int64_t)kl * N1 + l) * P.nsb + l / TS) * 4;
-    warp_sum_partials(rowP, l / TB + 1, colP, nf / TS - l / TS + 1, lane, out);
-}
-// I>(t_j, t_nf) from the partials of collision_kernel(nf), j < nf
-__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, int lane, cplx* out) {
-    const int N1 = P.n_steps + 1;
-    const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * N1 + j) * P.nbb * 4;
-    warp_sum_partials(gcP, j / TB + 1, nullptr, 0, lane, out);
+// I>(t_j, t_nf), j < nf
+__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, cplx* out) {
+    const int64_t N1 = P.n_steps + 1;
+    const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * P.nbb * N1 + j) * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = cz();
+    const int nr = j / TB;
+#pragma unroll 4
+    for (int bc = 0; bc <= nr; ++bc)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], gcP[bc * N1 * 4 + c]);
 }
 
-// kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last); warp per point
+// kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last)
 __global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr, cplx* lc, cplx* gc) {
-    const int kl = blockIdx.y, lane = threadIdx.x & 31;
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int kl = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
     cplx v[4];
-    reduce_lr(P, kl, i, n, lane, v);
-    if (lane < 4) {
-        lr[((int64_t)kl * 4 + lane) * (n + 1) + i] = v[lane];
-        gr[((int64_t)kl * 4 + lane) * (n + 1) + i] = cneg(v[lane]);
+    reduce_lr(P, kl, i, n, v);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        lr[((int64_t)kl * 4 + c) * (n + 1) + i] = v[c];
+        gr[((int64_t)kl * 4 + c) * (n + 1) + i] = cneg(v[c]);
     }
     if (i < n) {
-        reduce_gc(P, kl, i, lane, v);
-        if (lane < 4) {
-            gc[((int64_t)kl * 4 + lane) * n + i] = v[lane];
-            lc[((int64_t)kl * 4 + lane) * n + i] = cneg(v[lane]);
+        reduce_gc(P, kl, i, v);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            gc[((int64_t)kl * 4 + c) * n + i] = v[c];
+            lc[((int64_t)kl * 4 + c) * n + i] = cneg(v[c]);
         }
     }
 }
@@ -721,9 +722,8 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
     mm_bdag(out, src, phi);
 }
 
-// One warp per frontier point b (b = n is the equal-time diagonal).  The warp
-// reduces the K2 partials cooperatively; every lane then holds identical
-// values, lanes 0..7 write one plane each.
+// One thread per frontier point b (b = n is the equal-time diagonal); Phi(t_{n-1/2}, k)
+// comes from the per-step table (built at init; rebuilt per iteration for hf_mode="on").
 __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int phase, int it) {
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
@@ -731,8 +731,8 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     } else if (kbe_skip(ctl, it, P.eps)) {
         return;
     }
-    const int kl = blockIdx.y, k = P.k_lo + kl;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kl = blockIdx.y;
+    const int nkl = P.k_hi - P.k_lo;
     __shared__ double red[4];
     __shared__ int redf[4];
     if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < KBE_MAX_ITER) {
@@ -740,10 +740,14 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         ctl->nonfinite[threadIdx.x] = 0;
     }
     cplx phi[4];
-    build_phi(P, ctl, n, k, phi);
+    {
+        const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[c] = ph[c];
+    }
     const double dt = P.dt;
     const int N1 = P.n_steps + 1;
-    const int b = blockIdx.x * 4 + warp;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
     cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
     const cplx* prev = G + slice_off(n - 1);
     const int64_t plp = plane_len(n - 1);
@@ -758,13 +762,14 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         if (phase == 0) {
             if (b < n) {
                 cplx lo[4], co[4], gl[4], gu[4];
-                reduce_lr(P, kl, b, n - 1, lane, lo);
-                if (b < n - 1) reduce_gc(P, kl, b, lane, co);
+                reduce_lr(P, kl, b, n - 1, lo);
+                if (b < n - 1) reduce_gc(P, kl, b, co);
                 else {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) co[c] = cneg(lo[c]);   // greater_row[n-1] = -lesser_row[n-1]
                 }
-                if (lane < 4) { lro[b * 4 + lane] = lo[lane]; clo[b * 4 + lane] = co[lane]; }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { lro[b * 4 + c] = lo[c]; clo[b * 4 + c] = co[c]; }
                 load_cell(prev, plp, b, gl, gu);
                 advance_row(phi, gl, lo, dt, nl);
                 advance_col(phi, gu, co, dt, nu);
@@ -784,8 +789,8 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             cplx lo[4], co[4], ln[4], gn[4], gl[4], gu[4], irow[4], icol[4], row[4], col[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { lo[c] = lro[bb * 4 + c]; co[c] = clo[bb * 4 + c]; }
-            reduce_lr(P, kl, bb, n, lane, ln);
-            reduce_gc(P, kl, bb, lane, gn);
+            reduce_lr(P, kl, bb, n, ln);
+            reduce_gc(P, kl, bb, gn);
             load_cell(prev, plp, bb, gl, gu);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -799,7 +804,7 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
                 for (int c = 0; c < 4; ++c) { nl[c] = row[c]; nu[c] = col[c]; }
             } else {
                 cplx lnn[4], ml[4], mg[4], src[4], d[4];
-                reduce_lr(P, kl, n, n, lane, lnn);
+                reduce_lr(P, kl, n, n, lnn);
                 neg_dag(ml, row);   // mirror of the fresh row entry (propagator.py:193)
                 neg_dag(mg, col);
                 // i_dl = (lesser_col[n-1] + lesser_row[n]) / 2, lesser_col = -greater_col
@@ -825,18 +830,26 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             res = absmax4(nu, ou, res);
             fin = finite4(nl) && finite4(nu);
         }
-        __syncwarp();
-        if (lane < 8) {
-            const cplx v = lane < 4 ? nl[lane & 3] : nu[lane & 3];
-            cur[lane * plc + b] = v;
-            if (P.front_send) {
-                const int64_t pm = plane_len(P.n_steps);
-                ((cplx*)P.front_send)[(int64_t)kl * 8 * pm + lane * pm + b] = v;
-            }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            cur[c * plc + b] = nl[c];
+            cur[(4 + c) * plc + b] = nu[c];
+        }
+        if (P.front_send) {
+            const int64_t pm = plane_len(P.n_steps);
+            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { fs[c * pm + b] = nl[c]; fs[(4 + c) * pm + b] = nu[c]; }
         }
     }
     if (phase == 1) {
-        if (lane == 0) { red[warp] = res; redf[warp] = fin ? 0 : 1; }
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double other = __shfl_xor_sync(0xffffffffu, res, o);
+            res = (res != res || other != other) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(res, other);
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, !fin);
+        if (lane == 0) { red[warp] = res; redf[warp] = ballot != 0; }
         __syncthreads();
         if (threadIdx.x == 0) {
             double r = red[0];
@@ -852,29 +865,54 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     }
 }
 
+// Phi(t_{n-1/2}, k) for steps n in [n0, n1], local k (hf term from ctl->hf_sum when hf_mode="on")
+__global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int check_skip) {
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (check_skip && kbe_skip(ctl, it, P.eps)) return;
+    const int nkl = P.k_hi - P.k_lo;
+    const int64_t total = (int64_t)(n1 - n0 + 1) * nkl;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = n0 + (int)(i / nkl), kl = (int)(i % nkl);
+        cplx phi[4];
+        build_phi(P, ctl, n, P.k_lo + kl, phi);
+        cplx* dst = (cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dst[c] = phi[c];
+    }
+}
+
 // hf_mode="on": k-sum of rho(t_{n-1}) (phase 0) or of (rho(t_{n-1}) + rho(t_n))/2 (phase 1)
 __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(ctl, it, P.eps)) return;
-    if (threadIdx.x != 0) return;
     const int nloc = P.k_hi - P.k_lo;
-    cplx acc[4] = {cz(), cz(), cz(), cz()};
-    for (int kl = 0; kl < nloc; ++kl) {
-        const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
-        const cplx* a = G + slice_off(n - 1);
-        const int64_t pa = plane_len(n - 1);
-        for (int c = 0; c < 4; ++c) {
-            const cplx g0 = a[c * pa + (n - 1)];
-            cplx r = make_double2(g0.y, -g0.x);   // rho = -i G<
-            if (phase == 1) {
-                const cplx* bcur = G + slice_off(n);
-                const cplx g1 = bcur[c * plane_len(n) + n];
-                r = cscale(cadd(r, make_double2(g1.y, -g1.x)), 0.5);
+    if (threadIdx.x == 0) {
+        cplx acc[4] = {cz(), cz(), cz(), cz()};
+        for (int kl = 0; kl < nloc; ++kl) {
+            const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+            const cplx* a = G + slice_off(n - 1);
+            const int64_t pa = plane_len(n - 1);
+            for (int c = 0; c < 4; ++c) {
+                const cplx g0 = a[c * pa + (n - 1)];
+                cplx r = make_double2(g0.y, -g0.x);   // rho = -i G<
+                if (phase == 1) {
+                    const cplx* bcur = G + slice_off(n);
+                    const cplx g1 = bcur[c * plane_len(n) + n];
+                    r = cscale(cadd(r, make_double2(g1.y, -g1.x)), 0.5);
+                }
+                acc[c] = cadd(acc[c], r);
             }
-            acc[c] = cadd(acc[c], r);
         }
+        for (int c = 0; c < 4; ++c) ctl->hf_sum[c] = acc[c];
     }
-    for (int c = 0; c < 4; ++c) ctl->hf_sum[c] = acc[c];
+    if (P.front_all) return;   // k-sharded: the host all-reduces hf_sum, then kbe_build_phi
+    __syncthreads();
+    for (int kl = threadIdx.x; kl < nloc; kl += blockDim.x) {
+        cplx phi[4];
+        build_phi(P, ctl, n, P.k_lo + kl, phi);
+        cplx* dst = (cplx*)P.phi + ((int64_t)n * nloc + kl) * 4;
+        for (int c = 0; c < 4; ++c) dst[c] = phi[c];
+    }
 }
 
 // =================================================================== K4: finish
@@ -1006,10 +1044,11 @@ static int check_problem(const kbe_problem* p) {
         snprintf(g_err, sizeof(g_err), "limit_mode 'langreth' is not implemented on the device path");
         return KBE_ERR_UNSUPPORTED;
     }
-    if (p->n_k > 256 && p->k_hi - p->k_lo > 256) {
-        snprintf(g_err, sizeof(g_err), "n_k_local > 256 not supported");
+    if (p->n_k > 128) {
+        snprintf(g_err, sizeof(g_err), "n_k > 128 is not supported by the fused Sigma kernel (one CTA per pair)");
         return KBE_ERR_UNSUPPORTED;
     }
+    if (!p->phi) { set_err("kbe_problem.phi", cudaSuccess); return KBE_ERR_ARG; }
     return KBE_OK;
 }
 
@@ -1034,6 +1073,9 @@ int kbe_init_history(const kbe_problem* p, void* stream) {
     const int nloc = p->k_hi - p->k_lo;
     init_slice0_kernel<<<(nloc + 127) / 128, 128, 0, st>>>(*p);
     KBE_CHECK_LAUNCH("init_slice0_kernel");
+    const int64_t cnt = (int64_t)p->n_steps * nloc;
+    phi_table_kernel<<<(int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096), 256, 0, st>>>(*p, 1, p->n_steps, 0, 0);
+    KBE_CHECK_LAUNCH("phi_table_kernel");
     return KBE_OK;
 }
 
@@ -1048,7 +1090,7 @@ int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream
     if ((rc = ensure_attrs())) return rc;
     const int pb = sigma_pairs_per_block(p->n_k);
     const int grid = (n + 1 + pb - 1) / pb;
-    sigma_frontier_kernel<<<grid, 256, sigma_smem_bytes(p->n_k, pb), (cudaStream_t)stream>>>(*p, n, it);
+    sigma_frontier_kernel<<<grid, sigma_threads(p->n_k), sigma_smem_bytes(p->n_k, pb), (cudaStream_t)stream>>>(*p, n, it);
     KBE_CHECK_LAUNCH("sigma_frontier_kernel");
     return KBE_OK;
 }
@@ -1088,7 +1130,7 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
                         void* greater_col, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    dim3 grid((n + 1 + 3) / 4, p->k_hi - p->k_lo);
+    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
     collision_slice_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, (cplx*)lesser_row, (cplx*)greater_row,
                                                                    (cplx*)lesser_col, (cplx*)greater_col);
     KBE_CHECK_LAUNCH("collision_slice_kernel");
@@ -1099,7 +1141,7 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    dim3 grid((n + 1 + 3) / 4, p->k_hi - p->k_lo);
+    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
     update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
     KBE_CHECK_LAUNCH("update_kernel");
     return KBE_OK;
@@ -1108,8 +1150,17 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
 int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    hf_mean_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
+    hf_mean_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
     KBE_CHECK_LAUNCH("hf_mean_kernel");
+    return KBE_OK;
+}
+
+int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 1 || n > p->n_steps) { set_err("kbe_build_phi: n", cudaSuccess); return KBE_ERR_ARG; }
+    phi_table_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(*p, n, n, it, 1);
+    KBE_CHECK_LAUNCH("phi_table_kernel");
     return KBE_OK;
 }
 

@@ -112,6 +112,7 @@ class _Workspace:
         self.col_old = torch.zeros((kl, N1, 4), **c128)
         self.ctl = torch.zeros(int(_lib.lib().kbe_ctl_bytes()), dtype=torch.uint8, device=device)
         self.reports = torch.zeros((N1, _lib.REPORT_W), dtype=torch.float64, device=device)
+        self.phi = torch.zeros((N1, kl, 4), **c128)
         self.eps_v = as_device_f64(eps_v, device)
         self.eps_c = as_device_f64(eps_c, device)
         self.u_table = as_device_f64(u_table, device)
@@ -138,6 +139,7 @@ class _Workspace:
         p.front_send = self.front_send.data_ptr() if self.front_send is not None else None
         p.front_all = self.front_all.data_ptr() if self.front_all is not None else None
         p.ctl, p.reports = self.ctl.data_ptr(), self.reports.data_ptr()
+        p.phi = self.phi.data_ptr()
         self.problem = p
 
     def problem_ptr(self) -> int:
@@ -257,6 +259,7 @@ class PropagationDriver:
         if self.model.hf_mode == "on":
             chk(L.kbe_hf_mean(P, n, 0, 0, st), "kbe_hf_mean")
             self._allreduce_hf()
+            chk(L.kbe_build_phi(P, n, 0, st), "kbe_build_phi")
         chk(L.kbe_update(P, n, 0, 0, st), "kbe_update")
         self._gather_frontier()
         for it in range(self.cfg.max_iter):
@@ -266,6 +269,7 @@ class PropagationDriver:
             if self.model.hf_mode == "on":
                 chk(L.kbe_hf_mean(P, n, 1, it, st), "kbe_hf_mean")
                 self._allreduce_hf()
+                chk(L.kbe_build_phi(P, n, it, st), "kbe_build_phi")
             chk(L.kbe_update(P, n, 1, it, st), "kbe_update")
             self._allreduce_ctl(it)
             self._gather_frontier()
