@@ -31,6 +31,8 @@ struct kbe_ctl {
     int poisoned;                          // step that produced a non-finite frontier
     int pad;
     cplx hf_sum[4];                        // k-sum of rho for hf_mode="on"
+    unsigned task_next;                    // collision work queue head (reset by the last CTA)
+    unsigned task_done;
 };
 
 static char g_err[512] = "";
@@ -447,152 +449,179 @@ __device__ __forceinline__ void tri_decode(int t, int& sc, int& bc) {
     bc = t - s * (s + 1) / 2;
 }
 
-// One warp = one task of 32 history points x 32 slices; no CTA-level barriers,
-// a 3-stage TMA bulk-copy ring per warp keeps ~8 KB per warp in flight.
+// One warp = one task of 32 history points x 32 slices; a persistent grid of 1-warp
+// CTAs walks the task list (tasks of both triangles, all local k).  No CTA-level
+// barriers; a 3-stage TMA bulk-copy ring per warp keeps ~8 KB per warp in flight.
+// A converged iteration costs one tiny grid of early exits.
 __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
-    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
-    const int part = blockIdx.y, kl = blockIdx.z;
-    const int smax = part == 0 ? n : n - 1;
-    if (smax < 0) return;
-    const int T = smax / TS + 1;
-    if ((int)blockIdx.x >= T * (T + 1) / 2) return;
-    int sc, bc;
-    tri_decode(blockIdx.x, sc, bc);
-    const int s0 = sc * TS, s1 = min(s0 + TS - 1, smax);
-    const int wb0 = bc * TB;            // wb0 <= s0: every slice has lane 0 valid
-    const int m = s1 - s0 + 1;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
-    const int b = wb0 + lane;
     const int N1 = P.n_steps + 1;
     const double dt = P.dt;
-
-    const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
-    const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-    const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
-    const cplx* hist = part == 0 ? S : G;                   // streamed triangle
-    const int64_t pln = plane_len(n);
+    const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
+    const int tri0 = T0 * (T0 + 1) / 2, tri1 = T1 * (T1 + 1) / 2;
+    const int per_k = tri0 + tri1;
+    const int total = per_k * (P.k_hi - P.k_lo);
     uint64_t* bars = sm.bar;
     if (lane == 0) {
         for (int i = 0; i < KBE_STAGES; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
     }
     __syncwarp();
-    if (lane == 0)
-        for (int i = 0; i < KBE_STAGES && i < m; ++i) issue_slice(hist, s0 + i, wb0, sm.buf[i], &bars[i]);
-    double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
-
-    if (part == 0) {
-        // per-slice vectors w_s A(s), w_s B(s);  A(s) = G>(t_n,t_s), B(s) = G<(t_n,t_s)
-        if (lane < m) {
-            const int s = s0 + lane;
-            const double w = quad_w(n, s, dt, P.quad);
-            cplx u[4], l[4], a[4];
-            load_cell(fr, pln, s, l, u);
-            if (s < n) neg_dag(a, u);
-            else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) a[c] = u[c];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = cscale(a[c], w); sm.vec[lane][4 + c] = cscale(l[c], w); }
-        }
-        cplx Ab[4], Bb[4], col[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { Ab[c] = cz(); Bb[c] = cz(); col[c] = cz(); }
-        if (b <= s1) {
-            const double w = quad_w(n, b, dt, P.quad);
-            cplx u[4], l[4];
-            load_cell(fr, pln, b, l, u);
-            if (b < n) neg_dag(Ab, u);
-            else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) Ab[c] = u[c];
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
-        }
+    unsigned gcount = 0;   // slices consumed by this CTA so far (ring position / parity)
+    for (;;) {
+        // dynamic work queue: balances the half-full diagonal tasks
+        unsigned tk = 0;
+        if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
+        const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
+        if (task >= total) break;
+        const int kl = task / per_k, r = task % per_k;
+        const int part = r < tri0 ? 0 : 1;
+        int sc, bc;
+        tri_decode(part == 0 ? r : r - tri0, sc, bc);
+        const int smax = part == 0 ? n : n - 1;
+        const int s0 = sc * TS, s1 = min(s0 + TS - 1, smax);
+        const int wb0 = bc * TB;            // wb0 <= s0: every slice has lane 0 valid
+        const int m = s1 - s0 + 1;
+        const int b = wb0 + lane;
+        const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+        const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
+        const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
+        const cplx* hist = part == 0 ? S : G;                   // streamed triangle
+        const int64_t pln = plane_len(n);
         __syncwarp();
-        for (int i = 0; i < m; ++i) {
-            const int s = s0 + i, st = i % KBE_STAGES;
-            mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
-            cplx SL[4], SU[4];
+        if (lane == 0)
+            for (int i = 0; i < KBE_STAGES && i < m; ++i) {
+                const unsigned st = (gcount + i) % KBE_STAGES;
+                issue_slice(hist, s0 + i, wb0, sm.buf[st], &bars[st]);
+            }
+        double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
+
+        if (part == 0) {
+            // per-slice vectors w_s A(s), w_s B(s);  A(s) = G>(t_n,t_s), B(s) = G<(t_n,t_s)
+            if (lane < m) {
+                const int s = s0 + lane;
+                const double w = quad_w(n, s, dt, P.quad);
+                cplx u[4], l[4], a[4];
+                load_cell(fr, pln, s, l, u);
+                if (s < n) neg_dag(a, u);
+                else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[st][c][lane]; SU[c] = sm.buf[st][4 + c][lane]; }
-            cplx row[4];
+                    for (int c = 0; c < 4; ++c) a[c] = u[c];
+                }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) row[c] = cz();
-            if (b <= s) {
-                mm_acc(row, Ab, SU);
-                if (b < s) {
-                    mm_bdag_acc(row, Bb, SL);
-                    cplx As[4], Bs[4];
+                for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = cscale(a[c], w); sm.vec[lane][4 + c] = cscale(l[c], w); }
+            }
+            cplx Ab[4], Bb[4], col[4];
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) { As[c] = sm.vec[i][c]; Bs[c] = sm.vec[i][4 + c]; }
-                    mm_bdag_acc(col, As, SU);   // col += As SU^dag + Bs SL
-                    mm_acc(col, Bs, SL);
-                } else {
+            for (int c = 0; c < 4; ++c) { Ab[c] = cz(); Bb[c] = cz(); col[c] = cz(); }
+            if (b <= s1) {
+                const double w = quad_w(n, b, dt, P.quad);
+                cplx u[4], l[4];
+                load_cell(fr, pln, b, l, u);
+                if (b < n) neg_dag(Ab, u);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) Ab[c] = u[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
+            }
+            __syncwarp();
+            for (int i = 0; i < m; ++i, ++gcount) {
+                const int s = s0 + i;
+                const unsigned st = gcount % KBE_STAGES;
+                mbar_wait(&bars[st], (gcount / KBE_STAGES) & 1u);
+                cplx SL[4], SU[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[st][c][lane]; SU[c] = sm.buf[st][4 + c][lane]; }
+                cplx row[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) row[c] = cz();
+                if (b <= s) {
+                    mm_acc(row, Ab, SU);
+                    if (b < s) {
+                        mm_bdag_acc(row, Bb, SL);
+                        cplx As[4], Bs[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) { As[c] = sm.vec[i][c]; Bs[c] = sm.vec[i][4 + c]; }
+                        mm_bdag_acc(col, As, SU);   // col += As SU^dag + Bs SL
+                        mm_acc(col, Bs, SL);
+                    } else {
+                        cplx t[4];
+                        mm(t, Bb, SL);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) row[c] = csub(row[c], t[c]);
+                    }
+                }
+                double v[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
+                const double rr = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
+                if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)] = rr;
+                // refill stage st only after every lane has consumed it (WAR across proxies)
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
+            }
+            if (b <= s1) {
+                cplx* colP = (cplx*)P.col_part;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c] = cneg(col[c]);
+            }
+        } else {
+            // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
+            cplx X[4], Y[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
+            if (b <= s1) load_cell(fr, pln, b, X, Y);
+            for (int i = 0; i < m; ++i, ++gcount) {
+                const int j = s0 + i;
+                const unsigned st = gcount % KBE_STAGES;
+                mbar_wait(&bars[st], (gcount / KBE_STAGES) & 1u);
+                cplx GL[4], GU[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[st][c][lane]; GU[c] = sm.buf[st][4 + c][lane]; }
+                cplx acc[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] = cz();
+                if (b <= j) {
+                    const double w = quad_w(j, b, dt, P.quad);
                     cplx t[4];
-                    mm(t, Bb, SL);
+                    mm_bdag(t, GL, X);                 // GL X^dag
+                    if (b < j) {
+                        mm_adag_acc(acc, GU, Y);       // GU^dag Y
+                    } else {
+                        cplx u[4];
+                        mm(u, GU, Y);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) row[c] = csub(row[c], t[c]);
+                        for (int c = 0; c < 4; ++c) acc[c] = cneg(u[c]);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[c] = cscale(csub(acc[c], t[c]), w);
                 }
+                double v[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
+                const double rr = warp_rs8(v, lane);
+                if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)] = rr;
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
             }
-            double v[8];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
-            const double r = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
-            if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)] = r;
-            // refill stage st only after every lane has consumed it (WAR across proxies)
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
         }
-        if (b <= s1) {
-            cplx* colP = (cplx*)P.col_part;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c] = cneg(col[c]);
-        }
-    } else {
-        // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
-        cplx X[4], Y[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
-        if (b <= s1) load_cell(fr, pln, b, X, Y);
-        for (int i = 0; i < m; ++i) {
-            const int j = s0 + i, st = i % KBE_STAGES;
-            mbar_wait(&bars[st], (uint32_t)((i / KBE_STAGES) & 1));
-            cplx GL[4], GU[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[st][c][lane]; GU[c] = sm.buf[st][4 + c][lane]; }
-            cplx acc[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc[c] = cz();
-            if (b <= j) {
-                const double w = quad_w(j, b, dt, P.quad);
-                cplx t[4];
-                mm_bdag(t, GL, X);                 // GL X^dag
-                if (b < j) {
-                    mm_adag_acc(acc, GU, Y);       // GU^dag Y
-                } else {
-                    cplx u[4];
-                    mm(u, GU, Y);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[c] = cneg(u[c]);
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc[c] = cscale(csub(acc[c], t[c]), w);
-            }
-            double v[8];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
-            const double r = warp_rs8(v, lane);
-            if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)] = r;
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
+    }
+    // last CTA out resets the queue for the next launch on this stream
+    if (lane == 0) {
+        __threadfence();
+        const unsigned d = atomicAdd(&ctl->task_done, 1u);
+        if (d == gridDim.x - 1) {
+            ctl->task_next = 0u;
+            ctl->task_done = 0u;
+            __threadfence();
         }
     }
 }
@@ -722,8 +751,12 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
     mm_bdag(out, src, phi);
 }
 
-// One thread per frontier point b (b = n is the equal-time diagonal); Phi(t_{n-1/2}, k)
-// comes from the per-step table (built at init; rebuilt per iteration for hf_mode="on").
+// K3: one CTA per group of 32 frontier points b (one k).  All points of an aligned
+// group share the same partial-chunk list, so the 128 threads (point o = tid/4,
+// block entry c = tid%4) sum the K2 partials with fully coalesced loads in a fixed
+// order; then each thread applies the predictor / corrector to its block entry.
+// The CTA holding b = n-1 also does the equal-time diagonal b = n.
+// Phi(t_{n-1/2}, k) comes from the per-step table (rebuilt per iteration for hf).
 __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int phase, int it) {
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
@@ -733,21 +766,54 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     }
     const int kl = blockIdx.y;
     const int nkl = P.k_hi - P.k_lo;
+    const int tid = threadIdx.x, o = tid >> 2, c = tid & 3;
+    const int grp = blockIdx.x, b0 = grp * 32, b = b0 + o;
+    const int64_t N1 = P.n_steps + 1;
+    const int nf = phase == 0 ? n - 1 : n;     // frontier of the collision being consumed
+    const bool diag_cta = grp == (n - 1) / 32;
+    __shared__ cplx sA[32][4], sB[32][4], sC[4], sRow[4], sCol[4];
     __shared__ double red[4];
     __shared__ int redf[4];
-    if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < KBE_MAX_ITER) {
-        ctl->res[threadIdx.x] = 0ull;
-        ctl->nonfinite[threadIdx.x] = 0;
+    if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid < KBE_MAX_ITER) {
+        ctl->res[tid] = 0ull;
+        ctl->nonfinite[tid] = 0;
     }
+    // ---- fixed-order partial sums: A = I<(t_nf, t_b), B = I>(t_b, t_nf)
+    {
+        const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
+        const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
+        const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
+        const int64_t cs = N1 * 4;   // chunk stride
+        cplx a = cz(), g = cz();
+        if (b < n) {
+#pragma unroll 8
+            for (int bc = 0; bc <= grp; ++bc) a = cadd(a, rowP[bc * cs]);
+#pragma unroll 8
+            for (int sc = grp; sc <= nf / TS; ++sc) a = cadd(a, colP[sc * cs]);
+            if (b < nf) {
+#pragma unroll 8
+                for (int bc = 0; bc <= grp; ++bc) g = cadd(g, gcP[bc * cs]);
+            }
+        }
+        sA[o][c] = a;
+        sB[o][c] = g;
+        if (phase == 1 && diag_cta && tid < 4) {   // C = I<(t_n, t_n)
+            const cplx* rp = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + n) * 4 + c;
+            const cplx* cp = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + n) * 4 + c;
+            cplx x = cz();
+            for (int bc = 0; bc <= n / TB; ++bc) x = cadd(x, rp[bc * cs]);
+            x = cadd(x, cp[(n / TS) * cs]);
+            sC[c] = x;
+        }
+    }
+    __syncthreads();
     cplx phi[4];
     {
         const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) phi[c] = ph[c];
+        for (int q = 0; q < 4; ++q) phi[q] = ph[q];
     }
     const double dt = P.dt;
-    const int N1 = P.n_steps + 1;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
     cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
     const cplx* prev = G + slice_off(n - 1);
     const int64_t plp = plane_len(n - 1);
@@ -755,112 +821,119 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     const int64_t plc = plane_len(n);
     cplx* lro = (cplx*)P.lr_old + ((int64_t)kl * N1) * 4;
     cplx* clo = (cplx*)P.col_old + ((int64_t)kl * N1) * 4;
+    cplx* fs = nullptr;
+    int64_t pm = 0;
+    if (P.front_send) {
+        pm = plane_len(P.n_steps);
+        fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
+    }
+    const int i = c >> 1, j = c & 1;
     double res = 0.0;
     bool fin = true;
-    if (b <= n) {
-        cplx nl[4], nu[4];   // new lower (G<(n,b)) / upper (G>(b,n)) blocks
+    if (b < n) {
+        // irow / icol: the collision blocks entering the row and column updates
+        auto IR = [&](int q) -> cplx {
+            return phase == 0 ? sA[o][q] : cscale(cadd(lro[b * 4 + q], sA[o][q]), 0.5);
+        };
+        auto IC = [&](int q) -> cplx {
+            if (phase == 0) return b < n - 1 ? sB[o][q] : cneg(sA[o][q]);   // greater_row[n-1] = -lesser_row[n-1]
+            return cscale(cadd(clo[b * 4 + q], sB[o][q]), 0.5);
+        };
         if (phase == 0) {
-            if (b < n) {
-                cplx lo[4], co[4], gl[4], gu[4];
-                reduce_lr(P, kl, b, n - 1, lo);
-                if (b < n - 1) reduce_gc(P, kl, b, co);
-                else {
+            lro[b * 4 + c] = IR(c);
+            clo[b * 4 + c] = IC(c);
+        }
+        // row(i,j) = sum_k Phi(i,k) [G<(n-1,b)(k,j) - i dt ir(k,j)]
+        // col(i,j) = sum_k [G>(b,n-1)(i,k) + i dt ic(i,k)] conj(Phi(j,k))
+        const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
+        cplx row = cz(), col = cz();
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) co[c] = cneg(lo[c]);   // greater_row[n-1] = -lesser_row[n-1]
-                }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { lro[b * 4 + c] = lo[c]; clo[b * 4 + c] = co[c]; }
-                load_cell(prev, plp, b, gl, gu);
-                advance_row(phi, gl, lo, dt, nl);
-                advance_col(phi, gu, co, dt, nu);
-            } else {
-                cplx gl[4], gu[4], t[4], d[4];
+        for (int k = 0; k < 2; ++k) {
+            const cplx gl = prev[(k * 2 + j) * plp + b];
+            row = cfma(ph[i * 2 + k], csub(gl, cmul_pi(IR(k * 2 + j), dt)), row);
+            const cplx gu = prev[(4 + i * 2 + k) * plp + b];
+            col = cfma_cb(cadd(gu, cmul_pi(IC(i * 2 + k), dt)), ph[j * 2 + k], col);
+        }
+        if (phase == 1) {
+            const cplx ol = cur[c * plc + b], ou = cur[(4 + c) * plc + b];
+            res = fmax(hypot(row.x - ol.x, row.y - ol.y), hypot(col.x - ou.x, col.y - ou.y));
+            if (res != res) res = __longlong_as_double(0x7ff8000000000000LL);
+            fin = isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
+            if (b == n - 1) { sRow[c] = row; sCol[c] = col; }
+        }
+        cur[c * plc + b] = row;
+        cur[(4 + c) * plc + b] = col;
+        if (fs) { fs[c * pm + b] = row; fs[(4 + c) * pm + b] = col; }
+    }
+    if (diag_cta) {
+        if (phase == 1) __syncthreads();   // sRow / sCol of point n-1
+        if (tid == 0) {
+            cplx nl[4], nu[4];
+            if (phase == 0) {
+                cplx gl[4], gu[4], tt[4], d[4];
                 load_cell(prev, plp, n - 1, gl, gu);
-                mm(t, phi, gl);
-                mm_bdag(d, t, phi);
+                mm(tt, phi, gl);
+                mm_bdag(d, tt, phi);
                 antiherm(nl, d);
-                mm(t, phi, gu);
-                mm_bdag(d, t, phi);
+                mm(tt, phi, gu);
+                mm_bdag(d, tt, phi);
                 antiherm(nu, d);
-            }
-        } else {
-            // corrector; b = n is the diagonal, which needs the new row/col at n-1
-            const int bb = b < n ? b : n - 1;
-            cplx lo[4], co[4], ln[4], gn[4], gl[4], gu[4], irow[4], icol[4], row[4], col[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { lo[c] = lro[bb * 4 + c]; co[c] = clo[bb * 4 + c]; }
-            reduce_lr(P, kl, bb, n, ln);
-            reduce_gc(P, kl, bb, gn);
-            load_cell(prev, plp, bb, gl, gu);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                irow[c] = cscale(cadd(lo[c], ln[c]), 0.5);
-                icol[c] = cscale(cadd(co[c], gn[c]), 0.5);
-            }
-            advance_row(phi, gl, irow, dt, row);
-            advance_col(phi, gu, icol, dt, col);
-            if (b < n) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { nl[c] = row[c]; nu[c] = col[c]; }
             } else {
-                cplx lnn[4], ml[4], mg[4], src[4], d[4];
-                reduce_lr(P, kl, n, n, lnn);
+                cplx row[4], col[4], ml[4], mg[4], src[4], d[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) { row[q] = sRow[q]; col[q] = sCol[q]; }
                 neg_dag(ml, row);   // mirror of the fresh row entry (propagator.py:193)
                 neg_dag(mg, col);
+                const int o1 = (n - 1) - b0;
                 // i_dl = (lesser_col[n-1] + lesser_row[n]) / 2, lesser_col = -greater_col
                 // i_dg = (greater_row[n-1] + greater_row[n]) / 2, greater_row = -lesser_row
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const cplx idl = cscale(cadd(cneg(gn[c]), lnn[c]), 0.5);
-                    src[c] = csub(ml[c], cmul_pi(idl, dt));
+                for (int q = 0; q < 4; ++q) {
+                    const cplx idl = cscale(cadd(cneg(sB[o1][q]), sC[q]), 0.5);
+                    src[q] = csub(ml[q], cmul_pi(idl, dt));
                 }
                 mm(d, phi, src);
                 antiherm(nl, d);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const cplx idg = cscale(cadd(cneg(ln[c]), cneg(lnn[c])), 0.5);
-                    src[c] = cadd(mg[c], cmul_pi(idg, dt));
+                for (int q = 0; q < 4; ++q) {
+                    const cplx idg = cscale(cadd(cneg(sA[o1][q]), cneg(sC[q])), 0.5);
+                    src[q] = cadd(mg[q], cmul_pi(idg, dt));
                 }
                 mm_bdag(d, src, phi);
                 antiherm(nu, d);
+                cplx ol[4], ou[4];
+                load_cell(cur, plc, n, ol, ou);
+                res = absmax4(nl, ol, res);
+                res = absmax4(nu, ou, res);
+                fin = fin && finite4(nl) && finite4(nu);
             }
-            cplx ol[4], ou[4];
-            load_cell(cur, plc, b, ol, ou);
-            res = absmax4(nl, ol, res);
-            res = absmax4(nu, ou, res);
-            fin = finite4(nl) && finite4(nu);
-        }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            cur[c * plc + b] = nl[c];
-            cur[(4 + c) * plc + b] = nu[c];
-        }
-        if (P.front_send) {
-            const int64_t pm = plane_len(P.n_steps);
-            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) { fs[c * pm + b] = nl[c]; fs[(4 + c) * pm + b] = nu[c]; }
+            for (int q = 0; q < 4; ++q) {
+                cur[q * plc + n] = nl[q];
+                cur[(4 + q) * plc + n] = nu[q];
+                if (fs) { fs[q * pm + n] = nl[q]; fs[(4 + q) * pm + n] = nu[q]; }
+            }
         }
     }
     if (phase == 1) {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        for (int o = 16; o > 0; o >>= 1) {
-            const double other = __shfl_xor_sync(0xffffffffu, res, o);
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int off = 16; off > 0; off >>= 1) {
+            const double other = __shfl_xor_sync(0xffffffffu, res, off);
             res = (res != res || other != other) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(res, other);
         }
         const unsigned ballot = __ballot_sync(0xffffffffu, !fin);
         if (lane == 0) { red[warp] = res; redf[warp] = ballot != 0; }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             double r = red[0];
-            int nf = redf[0];
-            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            int nfl = redf[0];
+            for (int w = 1; w < 4; ++w) {
                 r = (r != r || red[w] != red[w]) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(r, red[w]);
-                nf |= redf[w];
+                nfl |= redf[w];
             }
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
             atomicMax(&ctl->res[it], bits);
-            if (nf) atomicOr(&ctl->nonfinite[it], 1);
+            if (nfl) atomicOr(&ctl->nonfinite[it], 1);
         }
     }
 }
@@ -1022,12 +1095,20 @@ __global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int 
 
 // =================================================================== host side
 static bool g_attr_done = false;
+static int g_num_sms = 148;
+static int g_coll_occ = 8;   // resident collision CTAs per SM (occupancy API)
 static int ensure_attrs() {
     if (g_attr_done) return KBE_OK;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, collision_kernel, 32, sizeof(CollSmem));
+    if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
+    g_coll_occ = occ;
     e = cudaFuncSetAttribute(sigma_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_slice)", e); return KBE_ERR_CUDA; }
     g_attr_done = true;
@@ -1119,8 +1200,10 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
-    const int T = n / TS + 1;
-    dim3 grid(T * (T + 1) / 2, 2, p->k_hi - p->k_lo);
+    const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
+    const int64_t total = (int64_t)(T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * (p->k_hi - p->k_lo);
+    const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
+    const int grid = (int)(total < cap ? total : cap);
     collision_kernel<<<grid, 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
     KBE_CHECK_LAUNCH("collision_kernel");
     return KBE_OK;
@@ -1141,7 +1224,7 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
+    dim3 grid((n + 31) / 32, p->k_hi - p->k_lo);
     update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
     KBE_CHECK_LAUNCH("update_kernel");
     return KBE_OK;
