@@ -414,11 +414,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+// L2 policies: the history stream is read once per evaluation (evict first); the
+// K2 -> K3 partial sums must survive that stream in L2 (evict last).
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep2(cplx* p, cplx v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 
 #define KBE_STAGES 3
@@ -430,14 +449,15 @@ struct CollSmem {
 };
 
 // Issue the 8 plane copies of slice s, points [wb0, wb0+32) clipped to the plane.
-__device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar) {
+__device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
+                                            uint64_t pol) {
     const int64_t pl = plane_len(s);
     const int cnt = (int)min((int64_t)32, pl - wb0);
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_expect_tx(bar, 8u * bytes);
     const cplx* base = hist + slice_off(s) + wb0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar);
+    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar, pol);
 }
 
 // triangular index t -> (sc, bc) with 0 <= bc <= sc
@@ -471,6 +491,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         mbar_fence_init();
     }
     __syncwarp();
+    const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
     unsigned gcount = 0;   // slices consumed by this CTA so far (ring position / parity)
     for (;;) {
         // dynamic work queue: balances the half-full diagonal tasks
@@ -496,7 +517,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         if (lane == 0)
             for (int i = 0; i < KBE_STAGES && i < m; ++i) {
                 const unsigned st = (gcount + i) % KBE_STAGES;
-                issue_slice(hist, s0 + i, wb0, sm.buf[st], &bars[st]);
+                issue_slice(hist, s0 + i, wb0, sm.buf[st], &bars[st], pol_stream);
             }
         double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
 
@@ -561,16 +582,16 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
                 const double rr = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
-                if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)] = rr;
+                if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
                 // refill stage st only after every lane has consumed it (WAR across proxies)
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
+                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st], pol_stream);
             }
             if (b <= s1) {
                 cplx* colP = (cplx*)P.col_part;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c] = cneg(col[c]);
+                for (int c = 0; c < 4; ++c) st_keep2(&colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c], cneg(col[c]), pol_keep);
             }
         } else {
             // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
@@ -607,10 +628,10 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
                 const double rr = warp_rs8(v, lane);
-                if ((lane & 3) == 0) outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)] = rr;
+                if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)], rr, pol_keep);
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st]);
+                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st], pol_stream);
             }
         }
     }
@@ -766,19 +787,22 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     }
     const int kl = blockIdx.y;
     const int nkl = P.k_hi - P.k_lo;
-    const int tid = threadIdx.x, o = tid >> 2, c = tid & 3;
-    const int grp = blockIdx.x, b0 = grp * 32, b = b0 + o;
+    // thread = (point o, block entry c, chunk lane q): 8 x 4 x 4 = 128 threads; a CTA
+    // covers 8 points of one aligned group of 32 (all share one chunk list)
+    const int tid = threadIdx.x, q4 = tid & 3, c = (tid >> 2) & 3, o = tid >> 4;
+    const int grp = blockIdx.x >> 2, b0 = grp * 32 + (blockIdx.x & 3) * 8, b = b0 + o;
     const int64_t N1 = P.n_steps + 1;
     const int nf = phase == 0 ? n - 1 : n;     // frontier of the collision being consumed
-    const bool diag_cta = grp == (n - 1) / 32;
-    __shared__ cplx sA[32][4], sB[32][4], sC[4], sRow[4], sCol[4];
+    const bool diag_cta = b0 <= n - 1 && n - 1 < b0 + 8;
+    __shared__ cplx sA[8][4], sB[8][4], sC[4], sRow[4], sCol[4];
     __shared__ double red[4];
     __shared__ int redf[4];
     if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid < KBE_MAX_ITER) {
         ctl->res[tid] = 0ull;
         ctl->nonfinite[tid] = 0;
     }
-    // ---- fixed-order partial sums: A = I<(t_nf, t_b), B = I>(t_b, t_nf)
+    // ---- fixed-order partial sums: A = I<(t_nf, t_b), B = I>(t_b, t_nf); chunk lane q4
+    // sums chunks q4, q4+4, ... in order, then a fixed 2-level shuffle tree combines lanes.
     {
         const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
         const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
@@ -786,24 +810,34 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         const int64_t cs = N1 * 4;   // chunk stride
         cplx a = cz(), g = cz();
         if (b < n) {
-#pragma unroll 8
-            for (int bc = 0; bc <= grp; ++bc) a = cadd(a, rowP[bc * cs]);
-#pragma unroll 8
-            for (int sc = grp; sc <= nf / TS; ++sc) a = cadd(a, colP[sc * cs]);
+            const int nr = grp + 1, ns = nf / TS - grp + 1;
+#pragma unroll 4
+            for (int i = q4; i < nr + ns; i += 4)
+                a = cadd(a, i < nr ? rowP[i * cs] : colP[(grp + i - nr) * cs]);
             if (b < nf) {
-#pragma unroll 8
-                for (int bc = 0; bc <= grp; ++bc) g = cadd(g, gcP[bc * cs]);
+#pragma unroll 4
+                for (int i = q4; i < nr; i += 4) g = cadd(g, gcP[i * cs]);
             }
         }
-        sA[o][c] = a;
-        sB[o][c] = g;
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+            a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
+            a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
+            g.x += __shfl_xor_sync(0xffffffffu, g.x, off);
+            g.y += __shfl_xor_sync(0xffffffffu, g.y, off);
+        }
+        if (q4 == 0) {
+            sA[o][c] = a;
+            sB[o][c] = g;
+        }
         if (phase == 1 && diag_cta && tid < 4) {   // C = I<(t_n, t_n)
-            const cplx* rp = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + n) * 4 + c;
-            const cplx* cp = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + n) * 4 + c;
+            const int cc = tid;
+            const cplx* rp = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + n) * 4 + cc;
+            const cplx* cp = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + n) * 4 + cc;
             cplx x = cz();
             for (int bc = 0; bc <= n / TB; ++bc) x = cadd(x, rp[bc * cs]);
             x = cadd(x, cp[(n / TS) * cs]);
-            sC[c] = x;
+            sC[cc] = x;
         }
     }
     __syncthreads();
@@ -830,7 +864,7 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     const int i = c >> 1, j = c & 1;
     double res = 0.0;
     bool fin = true;
-    if (b < n) {
+    if (b < n && q4 == 0) {
         // irow / icol: the collision blocks entering the row and column updates
         auto IR = [&](int q) -> cplx {
             return phase == 0 ? sA[o][q] : cscale(cadd(lro[b * 4 + q], sA[o][q]), 0.5);
@@ -1224,7 +1258,7 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    dim3 grid((n + 31) / 32, p->k_hi - p->k_lo);
+    dim3 grid((n + 7) / 8, p->k_hi - p->k_lo);
     update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
     KBE_CHECK_LAUNCH("update_kernel");
     return KBE_OK;

@@ -210,3 +210,46 @@ def test_capacity_errors():
     drv.run()
     with pytest.raises(kb.CapacityError):
         drv.step()
+
+
+# ------------------------------------------------------------------ the bench workload, full length
+def test_cfg2_full_propagation_matches_reference_golden():
+    """BASELINE configs[1] (n_k=16, 1000 steps, U=0.5) against the REAL reference run
+    in full (tests/golden/make_golden.py cfg2_full): final row/column, equal-time
+    diagonals and per-step observables <= 1e-10."""
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "traj_cfg2_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("traj_cfg2_full.npz not generated")
+    g = np.load(path)
+    N = int(g["n_steps"])
+    model = kb.ModelConfig(u_protocol=float(g["u"]), pulse_intensity=float(g["pulse_intensity"]),
+                           pulse_center=float(g["pulse_center"]))
+    drv = kb.PropagationDriver(kb.build_kgrid(int(g["n_k"])), model,
+                               kb.StepConfig(dt=float(g["dt"]), n_steps=N, memory_budget=1 << 40))
+    reps = drv.run()
+    sl = drv.state.slice_view(N).cpu().numpy()           # (k, 8, N+1): row G<(N, b), column G>(b, N)
+    row = sl[:, 0:4, :].reshape(-1, 2, 2, N + 1)
+    col = sl[:, 4:8, :].reshape(-1, 2, 2, N + 1)
+    assert rel_err(row, g["final_row_lesser"]) <= 1e-10
+    assert rel_err(col, g["final_col_greater"]) <= 1e-10
+    diag = np.stack([drv.state.slice_view(s)[:, 0:4, s].cpu().numpy() for s in range(N + 1)], axis=-1)
+    assert rel_err(diag.reshape(-1, 2, 2, N + 1), g["diag_lesser"]) <= 1e-10
+    np.testing.assert_allclose([r.density for r in reps], g["density"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose([r.anticommutation_drift for r in reps], g["drift"], rtol=0, atol=1e-10)
+    flips = np.sum(np.array([r.iterations for r in reps]) != g["iterations"])
+    assert flips <= N // 50
+
+
+def test_large_run_is_deterministic():
+    """Two propagations through the TMA pipeline and the work queue are bitwise equal."""
+    model = kb.ModelConfig(u_protocol=0.5, pulse_intensity=0.2, pulse_center=0.5)
+    cfg = kb.StepConfig(dt=0.02, n_steps=400, memory_budget=1 << 40)
+    a = kb.PropagationDriver(kb.build_kgrid(16), model, cfg)
+    ra = a.run()
+    b = kb.PropagationDriver(kb.build_kgrid(16), model, cfg)
+    rb = b.run()
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    assert torch.equal(a.state.hist, b.state.hist)
+    assert torch.equal(a.sigma.hist, b.sigma.hist)
