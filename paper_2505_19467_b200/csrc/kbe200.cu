@@ -1070,6 +1070,11 @@ __global__ void init_slice0_kernel(kbe_problem P) {
         cplx* g = (cplx*)P.g_hist + (int64_t)kl * P.tri;   // slice 0: plane_len(0) = 8
         g[0 * 8] = make_double2(0.0, 1.0);     // G<(0,0)_00 = i
         g[7 * 8] = make_double2(0.0, -1.0);    // G>(0,0)_11 = -i
+        if (P.front_send) {                     // slice 0 of the all-gather send buffer
+            const int64_t pm = plane_len(P.n_steps);
+            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
+            for (int c = 0; c < 8; ++c) fs[c * pm] = g[c * 8];
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         kbe_ctl* ctl = (kbe_ctl*)P.ctl;

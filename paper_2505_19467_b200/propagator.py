@@ -89,6 +89,57 @@ def cayley_propagator(h: np.ndarray, dt: float) -> np.ndarray:
     return phi
 
 
+def _backend() -> str:
+    import torch.distributed as dist
+    return dist.get_backend() if dist.is_initialized() else "none"
+
+
+def all_gather_device(out: torch.Tensor, inp: torch.Tensor) -> None:
+    """out = concat over ranks of inp (rank order = k order).  NCCL moves device
+    memory directly (NVLink); other backends (gloo, for tests) stage through the host."""
+    import torch.distributed as dist
+    o = torch.view_as_real(out) if out.is_complex() else out
+    i = torch.view_as_real(inp) if inp.is_complex() else inp
+    if _backend() == "nccl":
+        dist.all_gather_into_tensor(o.reshape(-1), i.reshape(-1))
+        return
+    parts = [torch.empty(i.numel(), dtype=i.dtype) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, i.reshape(-1).cpu())
+    o.reshape(-1).copy_(torch.cat(parts).to(o.device))
+
+
+def all_reduce_device(t: torch.Tensor, op) -> None:
+    import torch.distributed as dist
+    if _backend() == "nccl":
+        dist.all_reduce(t, op=op)
+        return
+    c = t.cpu()
+    dist.all_reduce(c, op=op)
+    t.copy_(c.to(t.device))
+
+
+def all_gather_list(t: torch.Tensor, world: int) -> list:
+    import torch.distributed as dist
+    if _backend() == "nccl":
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return parts
+    parts = [torch.empty_like(t, device="cpu") for _ in range(world)]
+    dist.all_gather(parts, t.cpu())
+    return parts
+
+
+def combine_reports(stacked: np.ndarray) -> np.ndarray:
+    """Per-rank StepReport rows (world, steps, W) -> global rows: drift is a max over
+    k, the density column a sum over k, the non-finite flag an OR; iteration counts
+    and residuals are already global (all-reduced every iteration)."""
+    out = stacked[0].copy()
+    out[:, 4] = stacked[:, :, 4].max(axis=0)
+    out[:, 5] = stacked[:, :, 5].sum(axis=0)
+    out[:, 6] = stacked[:, :, 6].max(axis=0)
+    return out
+
+
 class _Workspace:
     """Device buffers + the ``kbe_problem`` struct handed to the C ABI.
 
@@ -224,24 +275,19 @@ class PropagationDriver:
 
     # ------------------------------------------------------------------ multi-rank plumbing
     def _gather_frontier(self) -> None:
-        """All-gather the new G slice (local k) into the all-k frontier buffer (NCCL)."""
-        import torch.distributed as dist
-        ws = self.ws
-        dist.all_gather_into_tensor(ws.front_all.view(-1), ws.front_send.view(-1))
+        """All-gather the new G slice (local k) into the all-k frontier buffer."""
+        all_gather_device(self.ws.front_all, self.ws.front_send)
 
     def _allreduce_ctl(self, it: int) -> None:
-        """Global max of residual bits and non-finite flags for corrector iteration it."""
+        """Global max of residual bits and non-finite flags (same decision on every rank)."""
         import torch.distributed as dist
-        res = self.ws.ctl[: 8 * _lib.MAX_ITER].view(torch.int64)
-        dist.all_reduce(res, op=dist.ReduceOp.MAX)
-        nf = self.ws.ctl[8 * _lib.MAX_ITER: 12 * _lib.MAX_ITER].view(torch.int32)
-        dist.all_reduce(nf, op=dist.ReduceOp.MAX)
+        all_reduce_device(self.ws.ctl[: 8 * _lib.MAX_ITER].view(torch.int64), dist.ReduceOp.MAX)
+        all_reduce_device(self.ws.ctl[8 * _lib.MAX_ITER: 12 * _lib.MAX_ITER].view(torch.int32), dist.ReduceOp.MAX)
 
     def _allreduce_hf(self) -> None:
         import torch.distributed as dist
         off = 208   # offsetof(kbe_ctl, hf_sum): 128 res + 64 nonfinite + 8 poisoned/pad, 16-aligned
-        hf = self.ws.ctl[off: off + 64].view(torch.float64)
-        dist.all_reduce(hf, op=dist.ReduceOp.SUM)
+        all_reduce_device(self.ws.ctl[off: off + 64].view(torch.float64), dist.ReduceOp.SUM)
 
     def _launch_step(self, n: int) -> None:
         L, P, st = _lib.lib(), self.ws.problem_ptr(), stream_ptr()
@@ -277,17 +323,10 @@ class PropagationDriver:
 
     # ------------------------------------------------------------------ reports
     def _reports(self, n0: int, n1: int) -> np.ndarray:
-        rows = self.ws.reports[n0: n1 + 1]
+        rows = self.ws.reports[n0: n1 + 1].contiguous()
         if self.world > 1:
-            import torch.distributed as dist
-            parts = [torch.empty_like(rows) for _ in range(self.world)]
-            dist.all_gather(parts, rows.contiguous())
-            stacked = torch.stack(parts)                   # (world, steps, W)
-            out = stacked[0].clone()
-            out[:, 4] = stacked[:, :, 4].amax(dim=0)       # drift: max over k
-            out[:, 5] = stacked[:, :, 5].sum(dim=0)        # density: sum over k
-            out[:, 6] = stacked[:, :, 6].amax(dim=0)
-            rows = out
+            parts = all_gather_list(rows, self.world)
+            return combine_reports(np.stack([to_host(p) for p in parts]))
         return to_host(rows)
 
     def _to_report(self, row: np.ndarray) -> StepReport:
