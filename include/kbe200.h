@@ -60,7 +60,7 @@ typedef struct kbe_problem {
     int32_t k_hi;
     int32_t n_steps;      /* capacity N: slices 0..N                               */
     int32_t quad;         /* 0 trapezoid, 1 simpson (collision.py:31-61)           */
-    int32_t limit_mode;   /* 0 as-printed (1 langreth: not on the device path yet) */
+    int32_t limit_mode;   /* 0 as-printed, 1 langreth (collision.py:188-191, 211-219) */
     int32_t hf;           /* hf_mode == "on"                                       */
     int32_t max_iter;     /* corrector cap, <= KBE_MAX_ITER                         */
     int32_t interacting;  /* any(U != 0): Sigma is evaluated (propagator.py:265)   */
@@ -76,9 +76,9 @@ typedef struct kbe_problem {
     const double* u_table;/* [N+1] U on the grid (model.py:46-56)                  */
     const double* u_mid;  /* [N+1] U at the step-n midpoint (model.py:59-68)       */
     const double* amp;    /* [N+1] pulse amplitude at the step-n midpoint (88-103) */
-    void* row_part;       /* [k_local][N+1][nbb][4] complex: row-collision partials*/
-    void* col_part;       /* [k_local][N+1][nsb][4]                                */
-    void* gc_part;        /* [k_local][N+1][nbb][4]: column-collision partials     */
+    void* row_part;       /* [k_local][nbb][N+1][4] complex: I< row sums, per point chunk */
+    void* col_part;       /* [k_local][nsb][N+1][4]: I< row, column-direction sums       */
+    void* gc_part;        /* [k_local][nbb][N+1][4]: I> column sums, per point chunk     */
     void* lr_old;         /* [k_local][N+1][4]: I<(t_{n-1}, t_l) kept for the step */
     void* col_old;        /* [k_local][N+1][4]: I>(t_j, t_{n-1}) kept for the step */
     void* front_send;     /* NULL (1 rank) or [k_local][8][plane_len(N)]            */
@@ -86,6 +86,13 @@ typedef struct kbe_problem {
     void* ctl;            /* kbe_ctl_bytes() of device control state               */
     double* reports;      /* [N+1][KBE_REPORT_W]                                   */
     void* phi;            /* [N+1][k_local][4] complex: Cayley propagator per step */
+    /* limit_mode = langreth only (NULL otherwise): I> rows and I< columns are
+     * accumulated separately; the G pass also scatters along columns. */
+    void* row_part_g;     /* [k_local][nbb][N+1][4]: I> row sums                    */
+    void* col_part_g;     /* [k_local][nsb][N+1][4]: I> column-direction sums       */
+    void* lc_part;        /* [k_local][nbb][N+1][4]: I< column, row-direction sums  */
+    void* gc_part_c;      /* [k_local][nsb][N+1][4]: I> column, column-direction    */
+    void* lc_part_c;      /* [k_local][nsb][N+1][4]: I< column, column-direction    */
 } kbe_problem;
 
 /* ---- layout helpers (host-callable, no device work) ---------------------- */

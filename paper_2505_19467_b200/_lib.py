@@ -42,6 +42,7 @@ class KbeProblem(ctypes.Structure):
         ("lr_old", _p), ("col_old", _p),
         ("front_send", _p), ("front_all", _p),
         ("ctl", _p), ("reports", _p), ("phi", _p),
+        ("row_part_g", _p), ("col_part_g", _p), ("lc_part", _p), ("gc_part_c", _p), ("lc_part_c", _p),
     ]
 
 

@@ -22,7 +22,7 @@ from .state import _is_device_state, pack_history
 
 LIMIT_MODES = ("as-printed", "langreth")
 QUAD_KINDS = ("trapezoid", "simpson")
-DEVICE_LIMIT_MODES = ("as-printed",)
+DEVICE_LIMIT_MODES = ("as-printed", "langreth")
 
 
 def quadrature_weights(n: int, dt: float, kind: str = "trapezoid") -> np.ndarray:
@@ -98,7 +98,7 @@ def collision_frontier(state, sigma, n: int, rule: QuadratureRule = QuadratureRu
     Device states are read in place; reference-layout host arrays are packed
     into temporary device histories first.
     """
-    quad, _ = validate_rule(rule.kind, limit_mode)
+    quad, limit = validate_rule(rule.kind, limit_mode)
     if schedule is not None:
         schedule.validate(state.n_k_local)
     from .propagator import _Workspace
@@ -111,7 +111,7 @@ def collision_frontier(state, sigma, n: int, rule: QuadratureRule = QuadratureRu
         g_hist = pack_history(lesser, state.greater, n_steps, n)
         s_hist = pack_history(sigma.greater, sigma.lesser, n_steps, n)
     nk = g_hist.shape[0]
-    ws = _Workspace.for_collision(nk, n_steps, float(state.dt), quad, g_hist, s_hist, dev)
+    ws = _Workspace.for_collision(nk, n_steps, float(state.dt), quad, g_hist, s_hist, dev, limit)
     st = stream_ptr()
     L = _lib.lib()
     _lib.check(L.kbe_collision_frontier(ws.problem_ptr(), n, 0, st), "kbe_collision_frontier")

@@ -647,38 +647,262 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
     }
 }
 
+// K2, limit_mode = "langreth" (collision.py:188-191, 211-219): the second term's
+// quadrature limit is the column time t_l (rows) / t_n (columns), so I> != -I< and
+// both components are accumulated.  Same task decomposition and TMA ring as the
+// as-printed kernel; the G triangle now also runs over slice n and scatters its
+// second term along the column direction.
+//  Sigma triangle cell (s,b), Xc = S>(b,s) (= -SL^dag, or SL on the diagonal):
+//    I<_row[s] += w(n)_b D(b) SU + w(s)_b B(b) (SU - Xc)
+//    I>_row[s] += -w(n)_b D(b) Xc - w(s)_b A(b) (SU - Xc)
+//    I<_row[b] -= w(n)_s D(s) SU^dag,   I>_row[b] -= w(n)_s D(s) SL      (b < s)
+//    with D = A - B = G>(n,.) - G<(n,.)
+//  G triangle cell (s,b), Gg = G>(s,b) (= -GU^dag, or GU on the diagonal),
+//  Y(b) = S<(b,n), Z(b) = S>(b,n), V(s) = w(n)_s (Y(s) - Z(s)):
+//    I<_col[s] += w(s)_b (Gg - GL) Y(b) + w(n)_b GL (Y(b) - Z(b))
+//    I>_col[s] += w(s)_b (GL - Gg) Z(b) + w(n)_b Gg (Z(b) - Y(b))
+//    I<_col[b] -= GL^dag V(s),   I>_col[b] -= GU V(s)                     (b < s)
+__global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P, int n, int it) {
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (kbe_skip(ctl, it, P.eps)) return;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
+    const int lane = threadIdx.x;
+    const int N1 = P.n_steps + 1;
+    const double dt = P.dt;
+    const int T0 = n / TS + 1;
+    const int tri0 = T0 * (T0 + 1) / 2;
+    const int per_k = 2 * tri0;
+    const int total = per_k * (P.k_hi - P.k_lo);
+    uint64_t* bars = sm.bar;
+    if (lane == 0) {
+        for (int i = 0; i < KBE_STAGES; ++i) mbar_init(&bars[i], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    unsigned gcount = 0;
+    for (;;) {
+        unsigned tk = 0;
+        if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
+        const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
+        if (task >= total) break;
+        const int kl = task / per_k, r = task % per_k;
+        const int part = r < tri0 ? 0 : 1;
+        int sc, bc;
+        tri_decode(part == 0 ? r : r - tri0, sc, bc);
+        const int s0 = sc * TS, s1 = min(s0 + TS - 1, n);
+        const int wb0 = bc * TB;
+        const int m = s1 - s0 + 1;
+        const int b = wb0 + lane;
+        const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+        const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
+        const cplx* fr = (part == 0 ? G : S) + slice_off(n);
+        const cplx* hist = part == 0 ? S : G;
+        const int64_t pln = plane_len(n);
+        __syncwarp();
+        if (lane == 0)
+            for (int i = 0; i < KBE_STAGES && i < m; ++i) {
+                const unsigned st = (gcount + i) % KBE_STAGES;
+                issue_slice(hist, s0 + i, wb0, sm.buf[st], &bars[st], pol_stream);
+            }
+        // per-slice vector (4 complex): part 0 D(s) w(n)_s, part 1 V(s)
+        if (lane < m) {
+            const int s = s0 + lane;
+            const double w = quad_w(n, s, dt, P.quad);
+            cplx l[4], u[4], v[4];
+            load_cell(fr, pln, s, l, u);
+            if (part == 0) {
+                cplx a[4];
+                if (s < n) neg_dag(a, u);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) a[c] = u[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[c] = cscale(csub(a[c], l[c]), w);
+            } else {
+                cplx z[4];   // Z(s) = S>(s,n) = -SL(n,s)^dag (s < n) | SL(n,n)
+                if (s < n) neg_dag(z, l);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) z[c] = l[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) v[c] = cscale(csub(u[c], z[c]), w);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm.vec[lane][c] = v[c];
+        }
+        // own-point vectors
+        cplx P1[4], P2[4], P3[4], colL[4], colG[4];
+        double wnb = 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { P1[c] = cz(); P2[c] = cz(); P3[c] = cz(); colL[c] = cz(); colG[c] = cz(); }
+        if (b <= s1) {
+            cplx l[4], u[4];
+            load_cell(fr, pln, b, l, u);
+            wnb = quad_w(n, b, dt, P.quad);
+            if (part == 0) {   // P1 = A(b), P2 = B(b), P3 = w(n)_b D(b)
+                if (b < n) neg_dag(P1, u);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) P1[c] = u[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { P2[c] = l[c]; P3[c] = cscale(csub(P1[c], l[c]), wnb); }
+            } else {           // P1 = Y(b), P2 = Z(b), P3 = w(n)_b (Y(b) - Z(b))
+                if (b < n) neg_dag(P2, l);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) P2[c] = l[c];
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { P1[c] = u[c]; P3[c] = cscale(csub(u[c], P2[c]), wnb); }
+            }
+        }
+        __syncwarp();
+        double* outL = (double*)(part == 0 ? P.row_part : P.lc_part);
+        double* outG = (double*)(part == 0 ? P.row_part_g : P.gc_part);
+        for (int i = 0; i < m; ++i, ++gcount) {
+            const int s = s0 + i;
+            const unsigned st = gcount % KBE_STAGES;
+            mbar_wait(&bars[st], (gcount / KBE_STAGES) & 1u);
+            cplx LO[4], UP[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { LO[c] = sm.buf[st][c][lane]; UP[c] = sm.buf[st][4 + c][lane]; }
+            cplx rl[4], rg[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { rl[c] = cz(); rg[c] = cz(); }
+            if (b <= s) {
+                const double wsb = quad_w(s, b, dt, P.quad);
+                cplx V[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) V[c] = sm.vec[i][c];
+                if (part == 0) {
+                    // LO = SL(s,b), UP = SU(s,b);  Xc = S>(b,s)
+                    cplx Xc[4], Ml[4], t[4];
+                    if (b < s) neg_dag(Xc, LO);
+                    else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) Xc[c] = LO[c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) Ml[c] = csub(UP[c], Xc[c]);
+                    mm_acc(rl, P3, UP);                 // w(n)_b D(b) SU
+                    mm(t, P2, Ml);                      // B(b) (SU - Xc)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rl[c] = cadd(rl[c], cscale(t[c], wsb));
+                    mm(t, P3, Xc);                      // -w(n)_b D(b) Xc
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rg[c] = cneg(t[c]);
+                    mm(t, P1, Ml);                      // -w(s)_b A(b) (SU - Xc)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rg[c] = csub(rg[c], cscale(t[c], wsb));
+                    if (b < s) {
+                        mm_bdag_acc(colL, V, UP);       // D(s) SU^dag
+                        mm_acc(colG, V, LO);            // D(s) SL
+                    }
+                } else {
+                    // LO = GL(s,b), UP = GU(s,b);  Gg = G>(s,b)
+                    cplx Gg[4], t[4], d[4];
+                    if (b < s) neg_dag(Gg, UP);
+                    else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) Gg[c] = UP[c];
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) d[c] = csub(Gg[c], LO[c]);
+                    mm(t, d, P1);                       // (Gg - GL) Y(b)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rl[c] = cscale(t[c], wsb);
+                    mm_acc(rl, LO, P3);                 // w(n)_b GL (Y - Z)
+                    mm(t, d, P2);                       // -(Gg - GL) Z(b)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rg[c] = cneg(cscale(t[c], wsb));
+                    mm(t, Gg, P3);                      // -w(n)_b Gg (Y - Z)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) rg[c] = csub(rg[c], t[c]);
+                    if (b < s) {
+                        mm_adag_acc(colL, LO, V);       // GL^dag V(s)
+                        mm_acc(colG, UP, V);            // GU V(s)
+                    }
+                }
+            }
+            double v[8];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { v[2 * c] = rl[c].x; v[2 * c + 1] = rl[c].y; }
+            const double r1 = warp_rs8(v, lane);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { v[2 * c] = rg[c].x; v[2 * c + 1] = rg[c].y; }
+            const double r2 = warp_rs8(v, lane);
+            if ((lane & 3) == 0) {
+                const int64_t o = (((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2);
+                st_keep(&outL[o], r1, pol_keep);
+                st_keep(&outG[o], r2, pol_keep);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st], pol_stream);
+        }
+        if (b <= s1) {
+            cplx* cL = (cplx*)(part == 0 ? P.col_part : P.lc_part_c);
+            cplx* cG = (cplx*)(part == 0 ? P.col_part_g : P.gc_part_c);
+            const int64_t o = (((int64_t)kl * P.nsb + sc) * N1 + b) * 4;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                st_keep2(&cL[o + c], cneg(colL[c]), pol_keep);
+                st_keep2(&cG[o + c], cneg(colG[c]), pol_keep);
+            }
+        }
+    }
+    if (lane == 0) {
+        __threadfence();
+        const unsigned d = atomicAdd(&ctl->task_done, 1u);
+        if (d == gridDim.x - 1) {
+            ctl->task_next = 0u;
+            ctl->task_done = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // Fixed-order reductions of the partials written by collision_kernel(nf).
 // Partial planes are [k][chunk][point][4 complex], so consecutive points (threads)
 // read consecutive 64-byte blocks for every chunk.
-// I<(t_nf, t_l) = sum over b-chunks of the row sums + sum over s-chunks of the column sums
-__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+// sum_{bc <= l/TB} rowdir[bc][l] + sum_{l/TS <= sc <= nf/TS} coldir[sc][l]  (coldir may be null)
+__device__ __forceinline__ void reduce_chunks(const kbe_problem& P, const void* rowdir, const void* coldir, int kl,
+                                              int l, int nf, cplx* out) {
     const int64_t N1 = P.n_steps + 1;
-    const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + l) * 4;
-    const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + l) * 4;
 #pragma unroll
     for (int c = 0; c < 4; ++c) out[c] = cz();
+    const cplx* rp = (const cplx*)rowdir + ((int64_t)kl * P.nbb * N1 + l) * 4;
     const int nr = l / TB;
 #pragma unroll 4
     for (int bc = 0; bc <= nr; ++bc)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rowP[bc * N1 * 4 + c]);
-    const int s_hi = nf / TS;
+        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rp[bc * N1 * 4 + c]);
+    if (coldir) {
+        const cplx* cp = (const cplx*)coldir + ((int64_t)kl * P.nsb * N1 + l) * 4;
+        const int s_hi = nf / TS;
 #pragma unroll 4
-    for (int sc = l / TS; sc <= s_hi; ++sc)
+        for (int sc = l / TS; sc <= s_hi; ++sc)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], colP[sc * N1 * 4 + c]);
+            for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], cp[sc * N1 * 4 + c]);
+    }
 }
-// I>(t_j, t_nf), j < nf
-__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, cplx* out) {
-    const int64_t N1 = P.n_steps + 1;
-    const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * P.nbb * N1 + j) * 4;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) out[c] = cz();
-    const int nr = j / TB;
-#pragma unroll 4
-    for (int bc = 0; bc <= nr; ++bc)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], gcP[bc * N1 * 4 + c]);
+// I<(t_nf, t_l) / I>(t_nf, t_l) (rows) and I>(t_j, t_nf) / I<(t_j, t_nf) (columns)
+__device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+    reduce_chunks(P, P.row_part, P.col_part, kl, l, nf, out);
+}
+__device__ __forceinline__ void reduce_gr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
+    reduce_chunks(P, P.row_part_g, P.col_part_g, kl, l, nf, out);
+}
+__device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, int nf, cplx* out) {
+    reduce_chunks(P, P.gc_part, P.limit_mode ? P.gc_part_c : nullptr, kl, j, nf, out);
+}
+__device__ __forceinline__ void reduce_lc(const kbe_problem& P, int kl, int j, int nf, cplx* out) {
+    reduce_chunks(P, P.lc_part, P.lc_part_c, kl, j, nf, out);
 }
 
 // kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last)
@@ -686,19 +910,29 @@ __global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr,
     const int kl = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
-    cplx v[4];
+    cplx v[4], w[4];
     reduce_lr(P, kl, i, n, v);
+    if (P.limit_mode) reduce_gr(P, kl, i, n, w);
+    else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c] = cneg(v[c]);
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         lr[((int64_t)kl * 4 + c) * (n + 1) + i] = v[c];
-        gr[((int64_t)kl * 4 + c) * (n + 1) + i] = cneg(v[c]);
+        gr[((int64_t)kl * 4 + c) * (n + 1) + i] = w[c];
     }
     if (i < n) {
-        reduce_gc(P, kl, i, v);
+        reduce_gc(P, kl, i, n, v);
+        if (P.limit_mode) reduce_lc(P, kl, i, n, w);
+        else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) w[c] = cneg(v[c]);
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             gc[((int64_t)kl * 4 + c) * n + i] = v[c];
-            lc[((int64_t)kl * 4 + c) * n + i] = cneg(v[c]);
+            lc[((int64_t)kl * 4 + c) * n + i] = w[c];
         }
     }
 }
@@ -794,7 +1028,7 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
     const int64_t N1 = P.n_steps + 1;
     const int nf = phase == 0 ? n - 1 : n;     // frontier of the collision being consumed
     const bool diag_cta = b0 <= n - 1 && n - 1 < b0 + 8;
-    __shared__ cplx sA[8][4], sB[8][4], sC[4], sRow[4], sCol[4];
+    __shared__ cplx sA[8][4], sB[8][4], sC[4], sRow[4], sCol[4], sX[4], sY[4], sZ[4];
     __shared__ double red[4];
     __shared__ int redf[4];
     if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid < KBE_MAX_ITER) {
@@ -807,6 +1041,7 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
         const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
         const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
+        const cplx* gcC = P.limit_mode ? (const cplx*)P.gc_part_c + ((int64_t)kl * P.nsb * N1 + b) * 4 + c : nullptr;
         const int64_t cs = N1 * 4;   // chunk stride
         cplx a = cz(), g = cz();
         if (b < n) {
@@ -815,8 +1050,9 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             for (int i = q4; i < nr + ns; i += 4)
                 a = cadd(a, i < nr ? rowP[i * cs] : colP[(grp + i - nr) * cs]);
             if (b < nf) {
+                const int ng = gcC ? nr + ns : nr;   // langreth: + column-direction chunks
 #pragma unroll 4
-                for (int i = q4; i < nr; i += 4) g = cadd(g, gcP[i * cs]);
+                for (int i = q4; i < ng; i += 4) g = cadd(g, i < nr ? gcP[i * cs] : gcC[(grp + i - nr) * cs]);
             }
         }
 #pragma unroll
@@ -829,6 +1065,16 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         if (q4 == 0) {
             sA[o][c] = a;
             sB[o][c] = g;
+        }
+        if (diag_cta && P.limit_mode && tid == 32) {
+            // langreth: I> rows and I< columns are independent of I< rows / I> columns
+            if (phase == 0) {
+                reduce_gr(P, kl, n - 1, n - 1, sX);   // greater_row_old[n-1]
+            } else {
+                reduce_lc(P, kl, n - 1, n, sX);       // lesser_col[n-1]
+                reduce_gr(P, kl, n - 1, n, sY);       // greater_row[n-1]
+                reduce_gr(P, kl, n, n, sZ);           // greater_row[n]
+            }
         }
         if (phase == 1 && diag_cta && tid < 4) {   // C = I<(t_n, t_n)
             const int cc = tid;
@@ -870,7 +1116,10 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             return phase == 0 ? sA[o][q] : cscale(cadd(lro[b * 4 + q], sA[o][q]), 0.5);
         };
         auto IC = [&](int q) -> cplx {
-            if (phase == 0) return b < n - 1 ? sB[o][q] : cneg(sA[o][q]);   // greater_row[n-1] = -lesser_row[n-1]
+            if (phase == 0) {
+                if (b < n - 1) return sB[o][q];
+                return P.limit_mode ? sX[q] : cneg(sA[o][q]);   // greater_row[n-1] (= -lesser_row, as-printed)
+            }
             return cscale(cadd(clo[b * 4 + q], sB[o][q]), 0.5);
         };
         if (phase == 0) {
@@ -923,14 +1172,17 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
                 // i_dg = (greater_row[n-1] + greater_row[n]) / 2, greater_row = -lesser_row
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const cplx idl = cscale(cadd(cneg(sB[o1][q]), sC[q]), 0.5);
+                    const cplx lc1 = P.limit_mode ? sX[q] : cneg(sB[o1][q]);
+                    const cplx idl = cscale(cadd(lc1, sC[q]), 0.5);
                     src[q] = csub(ml[q], cmul_pi(idl, dt));
                 }
                 mm(d, phi, src);
                 antiherm(nl, d);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const cplx idg = cscale(cadd(cneg(sA[o1][q]), cneg(sC[q])), 0.5);
+                    const cplx gr1 = P.limit_mode ? sY[q] : cneg(sA[o1][q]);
+                    const cplx gr2 = P.limit_mode ? sZ[q] : cneg(sC[q]);
+                    const cplx idg = cscale(cadd(gr1, gr2), 0.5);
                     src[q] = cadd(mg[q], cmul_pi(idg, dt));
                 }
                 mm_bdag(d, src, phi);
@@ -1136,6 +1388,7 @@ __global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int 
 static bool g_attr_done = false;
 static int g_num_sms = 148;
 static int g_coll_occ = 8;   // resident collision CTAs per SM (occupancy API)
+static int g_lang_occ = 8;
 static int ensure_attrs() {
     if (g_attr_done) return KBE_OK;
     int dev = 0;
@@ -1144,7 +1397,12 @@ static int ensure_attrs() {
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
-    int occ = 0;
+    e = cudaFuncSetAttribute(collision_langreth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
+    if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision_langreth)", e); return KBE_ERR_CUDA; }
+    int occ = 0, occ2 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, collision_langreth_kernel, 32, sizeof(CollSmem));
+    if (e != cudaSuccess || occ2 < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(langreth)", e); return KBE_ERR_CUDA; }
+    g_lang_occ = occ2;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, collision_kernel, 32, sizeof(CollSmem));
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
@@ -1160,9 +1418,9 @@ static int check_problem(const kbe_problem* p) {
         set_err("kbe_problem", cudaSuccess);
         return KBE_ERR_ARG;
     }
-    if (p->limit_mode != 0) {
-        snprintf(g_err, sizeof(g_err), "limit_mode 'langreth' is not implemented on the device path");
-        return KBE_ERR_UNSUPPORTED;
+    if (p->limit_mode != 0 && (!p->row_part_g || !p->col_part_g || !p->lc_part || !p->gc_part_c || !p->lc_part_c)) {
+        snprintf(g_err, sizeof(g_err), "limit_mode 'langreth' needs the langreth partial buffers");
+        return KBE_ERR_ARG;
     }
     if (p->n_k > 128) {
         snprintf(g_err, sizeof(g_err), "n_k > 128 is not supported by the fused Sigma kernel (one CTA per pair)");
@@ -1243,7 +1501,14 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     const int64_t total = (int64_t)(T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * (p->k_hi - p->k_lo);
     const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
     const int grid = (int)(total < cap ? total : cap);
-    collision_kernel<<<grid, 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
+    if (p->limit_mode)
+    {
+        const int64_t tl = 2 * (int64_t)(T0 * (T0 + 1) / 2) * (p->k_hi - p->k_lo);
+        const int64_t cl = (int64_t)g_num_sms * g_lang_occ;
+        collision_langreth_kernel<<<(int)(tl < cl ? tl : cl), 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
+    }
+    else
+        collision_kernel<<<grid, 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
     KBE_CHECK_LAUNCH("collision_kernel");
     return KBE_OK;
 }

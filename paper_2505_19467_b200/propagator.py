@@ -164,6 +164,10 @@ class _Workspace:
         self.ctl = torch.zeros(int(_lib.lib().kbe_ctl_bytes()), dtype=torch.uint8, device=device)
         self.reports = torch.zeros((N1, _lib.REPORT_W), dtype=torch.float64, device=device)
         self.phi = torch.zeros((N1, kl, 4), **c128)
+        self.lang = None
+        if limit_mode:   # langreth: I> rows and I< columns kept separately, both directions
+            shapes = (self.nbb, self.nsb, self.nbb, self.nsb, self.nsb)   # row_g, col_g, lc, gc_c, lc_c
+            self.lang = [torch.zeros((kl, nb, N1, 4), **c128) for nb in shapes]
         self.eps_v = as_device_f64(eps_v, device)
         self.eps_c = as_device_f64(eps_c, device)
         self.u_table = as_device_f64(u_table, device)
@@ -191,6 +195,8 @@ class _Workspace:
         p.front_all = self.front_all.data_ptr() if self.front_all is not None else None
         p.ctl, p.reports = self.ctl.data_ptr(), self.reports.data_ptr()
         p.phi = self.phi.data_ptr()
+        if self.lang is not None:
+            (p.row_part_g, p.col_part_g, p.lc_part, p.gc_part_c, p.lc_part_c) = [t.data_ptr() for t in self.lang]
         self.problem = p
 
     def problem_ptr(self) -> int:
@@ -198,10 +204,10 @@ class _Workspace:
 
     # --- small workspaces for the kernel-level API ------------------------------------
     @classmethod
-    def for_collision(cls, n_k, n_steps, dt, quad, g_hist, s_hist, device):
+    def for_collision(cls, n_k, n_steps, dt, quad, g_hist, s_hist, device, limit_mode=0):
         z = np.zeros(max(n_k, n_steps + 1))
         return cls(n_k=n_k, k_lo=0, k_hi=n_k, n_steps=n_steps, dt=dt, eps=1e-9, max_iter=1, quad=quad,
-                   limit_mode=0, hf=False, interacting=True, dipole=0.0, eps_v=z[:n_k], eps_c=z[:n_k],
+                   limit_mode=limit_mode, hf=False, interacting=True, dipole=0.0, eps_v=z[:n_k], eps_c=z[:n_k],
                    u_table=z[: n_steps + 1], u_mid=z[: n_steps + 1], amp=z[: n_steps + 1],
                    g_hist=g_hist, s_hist=s_hist, device=device)
 

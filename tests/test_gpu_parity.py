@@ -76,13 +76,14 @@ class _Arrays:
 
 
 @pytest.mark.parametrize("kind", ["trapezoid", "simpson"])
+@pytest.mark.parametrize("mode", ["as-printed", "langreth"])
 @pytest.mark.parametrize("n", [0, 1, 2, 5, 8])
-def test_collision_matches_reference_golden(kind, n):
+def test_collision_matches_reference_golden(kind, mode, n):
     g = load_golden("collision.npz")
     state = _Arrays(g["GL"], g["GG"], float(g["dt"]))
     sigma = _Arrays(g["SL"], g["SG"])
-    c = kb.collision_frontier(state, sigma, n, kb.QuadratureRule(kind))
-    tag = f"{kind}_as-printed_{n}"
+    c = kb.collision_frontier(state, sigma, n, kb.QuadratureRule(kind), limit_mode=mode)
+    tag = f"{kind}_{mode}_{n}"
     for name, got in (("lr", c.lesser_row), ("gr", c.greater_row), ("lc", c.lesser_col), ("gc", c.greater_col)):
         want = g[f"{name}_{tag}"]
         assert got.shape == want.shape
@@ -111,23 +112,24 @@ def _random_sym_history(n_k, cap, seed):
 
 
 @pytest.mark.parametrize("kind", ["trapezoid", "simpson"])
+@pytest.mark.parametrize("mode", ["as-printed", "langreth"])
 @pytest.mark.parametrize("n", [31, 32, 33, 63, 64, 65, 127, 128, 200, 301])
-def test_collision_multi_tile_matches_oracle(kind, n):
+def test_collision_multi_tile_matches_oracle(kind, mode, n):
     """Task edges of K2 (32 slices x 32 points per warp) against the oracle."""
     n_k = 2
     GL, GG, SL, SG = _random_sym_history(n_k, n, seed=n)
-    c = kb.collision_frontier(_Arrays(GL, GG), _Arrays(SL, SG), n, kb.QuadratureRule(kind))
-    want = O.collision_frontier(GL, GG, SL, SG, n, 0.05, kind)
+    c = kb.collision_frontier(_Arrays(GL, GG), _Arrays(SL, SG), n, kb.QuadratureRule(kind), limit_mode=mode)
+    want = O.collision_frontier(GL, GG, SL, SG, n, 0.05, kind, mode)
     assert rel_err(c.lesser_row, want.lesser_row) <= 1e-12
     assert rel_err(c.greater_row, want.greater_row) <= 1e-12
     assert rel_err(c.lesser_col, want.lesser_col) <= 1e-12
     assert rel_err(c.greater_col, want.greater_col) <= 1e-12
 
 
-def test_langreth_is_rejected_loudly():
+def test_unknown_limit_mode_is_rejected():
     g = load_golden("collision.npz")
     with pytest.raises(kb.ConfigError):
-        kb.collision_frontier(_Arrays(g["GL"], g["GG"]), _Arrays(g["SL"], g["SG"]), 3, limit_mode="langreth")
+        kb.collision_frontier(_Arrays(g["GL"], g["GG"]), _Arrays(g["SL"], g["SG"]), 3, limit_mode="retarded")
 
 
 # ------------------------------------------------------------------ trajectories (reference goldens)
@@ -146,7 +148,7 @@ def _driver_from_fixture(g):
     return kb.PropagationDriver(kb.build_kgrid(int(g["n_k"])), model, cfg)
 
 
-TRAJ = ["traj_nk4_full.npz", "traj_hf.npz", "traj_simpson.npz", "traj_nk64_synth.npz",
+TRAJ = ["traj_nk4_full.npz", "traj_hf.npz", "traj_simpson.npz", "traj_langreth.npz", "traj_nk64_synth.npz",
         "traj_dimer.npz", "traj_free.npz", "traj_nk16.npz"]
 
 
