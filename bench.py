@@ -206,9 +206,9 @@ def _collision_roofline(kb, drv, hbm_peak):
         calls = [(n - 1, 0)] + [(n, it) for it in range(drv.cfg.max_iter)]
         if drv.world > 1:
             raise RuntimeError("roofline pass runs on one rank")
+        if n == 1 and drv.interactions_on:      # same launch sequence as kbe_step
+            _lib.check(L.kbe_sigma_frontier(P, 0, 0, sp))
         for ci, (nf, it) in enumerate(calls):
-            if drv.interactions_on:
-                _lib.check(L.kbe_sigma_frontier(P, nf, it, sp))
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
@@ -216,9 +216,9 @@ def _collision_roofline(kb, drv, hbm_peak):
             e1.record(st)
             ev.append((n, ci, nf, e0, e1))
             if ci == 0:
-                _lib.check(L.kbe_update(P, n, 0, 0, sp))
+                _lib.check(L.kbe_update_sigma(P, n, 0, 0, sp))
             else:
-                _lib.check(L.kbe_update(P, n, 1, it, sp))
+                _lib.check(L.kbe_update_sigma(P, n, 1, it, sp))
         _lib.check(L.kbe_finish_step(P, n, sp))
     t_total1.record(st)
     torch.cuda.synchronize()
@@ -289,8 +289,10 @@ def run_ours(args):
     iters = reps[:, 1].astype(int)
     dens = reps[:, 5] / CFG["n_k"]
     value = args.steps * N / secs
-    per_step_launches = (1 + cfg.max_iter) * (2 + (1 if drv.interactions_on else 0)) + 1
-    gpu_launches = args.steps * (N * per_step_launches + 1)
+    # kbe_step: (1 + max_iter) x (K2 collision, K3 update+Sigma) + K4 finish; step 1 adds
+    # the ground state's Sigma(0); each propagation adds kbe_init_history's 2 kernels
+    per_step_launches = (1 + cfg.max_iter) * 2 + 1
+    gpu_launches = args.steps * (N * per_step_launches + (1 if drv.interactions_on else 0) + 2)
 
     # e2e: public API with host inputs (model tables in, StepReports out)
     torch.cuda.synchronize()

@@ -43,7 +43,8 @@ extern "C" {
 
 #define KBE_MAX_ITER 16      /* StepConfig.max_iter ceiling on the device path */
 #define KBE_TILE_B 32        /* collision warp-task: history points            */
-#define KBE_TILE_S 32        /* collision warp-task: time slices               */
+#define KBE_TILE_S 32        /* collision tile: time slices (a warp task takes 8, 16 or 32 of them) */
+#define KBE_COL_CHUNK 8      /* column-direction partial slots: one per 8 slices */
 #define KBE_REPORT_W 24      /* doubles per StepReport row (8 + KBE_MAX_ITER)  */
 
 /* Report row layout (doubles):
@@ -65,7 +66,7 @@ typedef struct kbe_problem {
     int32_t max_iter;     /* corrector cap, <= KBE_MAX_ITER                         */
     int32_t interacting;  /* any(U != 0): Sigma is evaluated (propagator.py:265)   */
     int32_t nbb;          /* partial-sum columns per output: ceil((N+1)/TILE_B)    */
-    int32_t nsb;          /* partial-sum columns per output: ceil((N+1)/TILE_S)    */
+    int32_t nsb;          /* partial-sum columns per output: ceil((N+1)/KBE_COL_CHUNK) */
     int32_t pad0;
     double dt, eps, dipole_re, dipole_im;
     int64_t tri;          /* complex elements per k of one packed history          */
@@ -93,6 +94,13 @@ typedef struct kbe_problem {
     void* lc_part;        /* [k_local][nbb][N+1][4]: I< column, row-direction sums  */
     void* gc_part_c;      /* [k_local][nsb][N+1][4]: I> column, column-direction    */
     void* lc_part_c;      /* [k_local][nsb][N+1][4]: I< column, column-direction    */
+    /* Fresh Sigma frontier (NULL: none; one rank, U != 0 only): [k_local][8][plane_len(N)].
+     * kbe_update_sigma writes Sigma(t_n, .) of the G iterate it just produced here
+     * and moves the Sigma the collision just consumed into the history, so that
+     * the history always holds what the reference's SigmaHistory holds (Sigma of
+     * the last EVALUATED iterate) while kbe_collision_frontier(n >= 1) reads the
+     * Sigma frontier slice from this buffer. */
+    void* s_fresh;
 } kbe_problem;
 
 /* ---- layout helpers (host-callable, no device work) ---------------------- */
@@ -147,6 +155,12 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
  * h(k; t_{n-1/2}) (model.py:123-152). */
 int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
 
+/* kbe_update fused with evaluate_sigma_batched (selfenergy.py:261-325) of the
+ * updated frontier: the CTA that writes G(t_n, t_b) for all k of its points b
+ * evaluates the second-Born Sigma(t_n, t_b) of those pairs (+ the diagonal) in
+ * the same launch.  One rank only (all k local).  With U == 0 it is kbe_update. */
+int kbe_update_sigma(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
+
 /* k-mean of rho for hf_mode="on" (model.py:106-120): phase 0 uses
  * rho(t_{n-1}), phase 1 uses (rho(t_{n-1}) + rho(t_n))/2.  Local k sum;
  * the caller all-reduces across ranks before dividing (kbe_hf_finalize). */
@@ -163,7 +177,9 @@ int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream);
 int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream);
 
 /* One whole PropagationDriver.step() (propagator.py:316-382) on one rank:
- * Sigma(n-1), I(n-1), predictor, max_iter x (Sigma(n), I(n), corrector), finish. */
+ * Sigma(n-1), I(n-1), predictor, max_iter x (Sigma(n), I(n), corrector), finish.
+ * Sigma(n-1) and every Sigma(n) come out of kbe_update_sigma; only step 1 runs
+ * the standalone kbe_sigma_frontier for the ground state's Sigma(0). */
 int kbe_step(const kbe_problem* p, int32_t n, void* stream);
 
 /* Steps n_first..n_last (inclusive) back to back (PropagationDriver.run,

@@ -17,10 +17,13 @@
 #include <stdio.h>
 #include <string.h>
 #include <math.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 1
+#define KBE_ABI_VERSION 2
 
 typedef double2 cplx;
 
@@ -177,6 +180,17 @@ __device__ __forceinline__ bool kbe_skip(const kbe_ctl* ctl, int it, double eps)
     return false;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Step kernels are launched with programmatic stream serialization: the next
+// kernel's CTAs are scheduled while this one runs (hiding launch latency) and
+// block in griddepcontrol.wait until it has completed and flushed memory.  Every
+// step kernel therefore waits before its first dependent read (the control block
+// included) and triggers its dependents right away.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ warp reduction
 // Sum 8 doubles over the 32 lanes with a reduce-scatter butterfly (9 shuffles);
 // lane L ends up holding the total of value index (L >> 2) & 7.
@@ -259,6 +273,7 @@ static size_t sigma_smem_bytes(int nk, int pb) { return (size_t)24 * pb * nk * s
 //   lesser  (primary G<(b,n), reversed G>(n,b)) -> S<(t_b,t_n) = upper planes 4..7
 //   greater (primary G>(n,b), reversed G<(b,n)) -> S>(t_n,t_b) = lower planes 0..3
 __global__ void __launch_bounds__(1024) sigma_frontier_kernel(kbe_problem P, int n, int it) {
+    pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
     extern __shared__ cplx sm[];
@@ -440,6 +455,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Sub-tile height (slices per warp task) of the as-printed collision pass at
+// frontier n: tiles stay 32 x 32 (KBE_TILE_S x KBE_TILE_B) for the partial-sum
+// layout, but a warp takes ts = 8, 16 or 32 of a tile's slices, chosen so that a
+// launch has >= KBE_COLL_TASKS warp tasks (small frontiers would otherwise leave
+// most of the 148 SMs idle).  Column-direction partials are kept per ts-chunk in
+// KBE_COL_CHUNK-granular slots; the consumer (K3) derives the same ts from n.
+// langreth keeps ts = 32.
+#define KBE_COLL_TASKS 4096
+__host__ __device__ __forceinline__ int coll_tiles(int n, int nkl) {
+    const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
+    return (T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * nkl;
+}
+__host__ __device__ __forceinline__ int coll_ts(int n, int nkl, int limit_mode) {
+    if (limit_mode) return TS;
+    const int tiles = coll_tiles(n, nkl);
+    if (tiles >= KBE_COLL_TASKS) return 32;
+    if (2 * tiles >= KBE_COLL_TASKS) return 16;
+    return KBE_COL_CHUNK;
+}
+
 #define KBE_STAGES 3
 // dynamic shared memory of one collision warp-task
 struct CollSmem {
@@ -448,16 +483,36 @@ struct CollSmem {
     uint64_t bar[KBE_STAGES];
 };
 
+// A streamed triangle: slices live in the packed history, except that slice alt_s
+// may be redirected to a side buffer (the fresh Sigma frontier, see s_fresh).
+struct SliceSrc {
+    const cplx* hist;
+    const cplx* alt;   // NULL: no redirection
+    int alt_s;
+    int64_t alt_pl;    // plane stride of the side buffer
+};
 // Issue the 8 plane copies of slice s, points [wb0, wb0+32) clipped to the plane.
-__device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
+__device__ __forceinline__ void issue_slice(const SliceSrc& src, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
                                             uint64_t pol) {
     const int64_t pl = plane_len(s);
     const int cnt = (int)min((int64_t)32, pl - wb0);
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_expect_tx(bar, 8u * bytes);
-    const cplx* base = hist + slice_off(s) + wb0;
+    const bool redirect = src.alt && s == src.alt_s;
+    const cplx* base = (redirect ? src.alt : src.hist + slice_off(s)) + wb0;
+    const int64_t stride = redirect ? src.alt_pl : pl;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar, pol);
+    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * stride, bytes, bar, pol);
+}
+// Sigma frontier source of K2 at frontier n: the side buffer s_fresh (written by the
+// fused update, kbe_update_sigma) when present, else Sigma slice n of the history.
+__device__ __forceinline__ const cplx* sigma_front(const kbe_problem& P, int kl, int n, int64_t& pl) {
+    if (P.s_fresh && n >= 1) {
+        pl = plane_len(P.n_steps);
+        return (const cplx*)P.s_fresh + (int64_t)kl * 8 * pl;
+    }
+    pl = plane_len(n);
+    return (const cplx*)P.s_hist + (int64_t)kl * P.tri + slice_off(n);
 }
 
 // triangular index t -> (sc, bc) with 0 <= bc <= sc
@@ -474,6 +529,7 @@ __device__ __forceinline__ void tri_decode(int t, int& sc, int& bc) {
 // barriers; a 3-stage TMA bulk-copy ring per warp keeps ~8 KB per warp in flight.
 // A converged iteration costs one tiny grid of early exits.
 __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -483,7 +539,8 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
     const double dt = P.dt;
     const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
     const int tri0 = T0 * (T0 + 1) / 2, tri1 = T1 * (T1 + 1) / 2;
-    const int per_k = tri0 + tri1;
+    const int ts = coll_ts(n, P.k_hi - P.k_lo, 0), nsub = TS / ts;
+    const int per_k = (tri0 + tri1) * nsub;
     const int total = per_k * (P.k_hi - P.k_lo);
     uint64_t* bars = sm.bar;
     if (lane == 0) {
@@ -499,20 +556,24 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
         const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
         if (task >= total) break;
-        const int kl = task / per_k, r = task % per_k;
+        const int kl = task / per_k, r = task % per_k / nsub, sub = task % nsub;
         const int part = r < tri0 ? 0 : 1;
         int sc, bc;
         tri_decode(part == 0 ? r : r - tri0, sc, bc);
         const int smax = part == 0 ? n : n - 1;
-        const int s0 = sc * TS, s1 = min(s0 + TS - 1, smax);
+        const int s0 = sc * TS + sub * ts, s1 = min(s0 + ts - 1, smax);
+        if (s0 > smax) continue;            // empty sub-tile past the frontier
         const int wb0 = bc * TB;            // wb0 <= s0: every slice has lane 0 valid
         const int m = s1 - s0 + 1;
         const int b = wb0 + lane;
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        const cplx* fr = (part == 0 ? G : S) + slice_off(n);   // frontier slice n
-        const cplx* hist = part == 0 ? S : G;                   // streamed triangle
-        const int64_t pln = plane_len(n);
+        int64_t spl;
+        const cplx* sfr = sigma_front(P, kl, n, spl);
+        // frontier slice n (vector) and the streamed triangle
+        const cplx* fr = part == 0 ? G + slice_off(n) : sfr;
+        const int64_t pln = part == 0 ? plane_len(n) : spl;
+        const SliceSrc hist = part == 0 ? SliceSrc{S, sfr, n, spl} : SliceSrc{G, nullptr, -1, 0};
         __syncwarp();
         if (lane == 0)
             for (int i = 0; i < KBE_STAGES && i < m; ++i) {
@@ -591,7 +652,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
             if (b <= s1) {
                 cplx* colP = (cplx*)P.col_part;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) st_keep2(&colP[(((int64_t)kl * P.nsb + sc) * N1 + b) * 4 + c], cneg(col[c]), pol_keep);
+                for (int c = 0; c < 4; ++c) st_keep2(&colP[(((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4 + c], cneg(col[c]), pol_keep);
             }
         } else {
             // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
@@ -663,6 +724,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 //    I>_col[s] += w(s)_b (GL - Gg) Z(b) + w(n)_b Gg (Z(b) - Y(b))
 //    I<_col[b] -= GL^dag V(s),   I>_col[b] -= GU V(s)                     (b < s)
 __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P, int n, int it) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -697,9 +759,11 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
         const int b = wb0 + lane;
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        const cplx* fr = (part == 0 ? G : S) + slice_off(n);
-        const cplx* hist = part == 0 ? S : G;
-        const int64_t pln = plane_len(n);
+        int64_t spl;
+        const cplx* sfr = sigma_front(P, kl, n, spl);
+        const cplx* fr = part == 0 ? G + slice_off(n) : sfr;
+        const int64_t pln = part == 0 ? plane_len(n) : spl;
+        const SliceSrc hist = part == 0 ? SliceSrc{S, sfr, n, spl} : SliceSrc{G, nullptr, -1, 0};
         __syncwarp();
         if (lane == 0)
             for (int i = 0; i < KBE_STAGES && i < m; ++i) {
@@ -870,9 +934,11 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
 // Fixed-order reductions of the partials written by collision_kernel(nf).
 // Partial planes are [k][chunk][point][4 complex], so consecutive points (threads)
 // read consecutive 64-byte blocks for every chunk.
-// sum_{bc <= l/TB} rowdir[bc][l] + sum_{l/TS <= sc <= nf/TS} coldir[sc][l]  (coldir may be null)
+// sum_{bc <= l/TB} rowdir[bc][l] + sum_{l/ts <= sc <= nf/ts} coldir[sc][l]  (coldir may be null;
+// ts = the column chunk height the producing launch used, coll_ts(nf))
 __device__ __forceinline__ void reduce_chunks(const kbe_problem& P, const void* rowdir, const void* coldir, int kl,
                                               int l, int nf, cplx* out) {
+    const int ts = coll_ts(nf, P.k_hi - P.k_lo, P.limit_mode);
     const int64_t N1 = P.n_steps + 1;
 #pragma unroll
     for (int c = 0; c < 4; ++c) out[c] = cz();
@@ -884,9 +950,9 @@ __device__ __forceinline__ void reduce_chunks(const kbe_problem& P, const void* 
         for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], rp[bc * N1 * 4 + c]);
     if (coldir) {
         const cplx* cp = (const cplx*)coldir + ((int64_t)kl * P.nsb * N1 + l) * 4;
-        const int s_hi = nf / TS;
+        const int s_hi = nf / ts;
 #pragma unroll 4
-        for (int sc = l / TS; sc <= s_hi; ++sc)
+        for (int sc = l / ts; sc <= s_hi; ++sc)
 #pragma unroll
             for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], cp[sc * N1 * 4 + c]);
     }
@@ -907,6 +973,7 @@ __device__ __forceinline__ void reduce_lc(const kbe_problem& P, int kl, int j, i
 
 // kernel-level collision_frontier: partials -> CollisionSlice arrays (batch-last)
 __global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr, cplx* lc, cplx* gc) {
+    pdl_enter();
     const int kl = blockIdx.y;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
@@ -1006,206 +1073,316 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
     mm_bdag(out, src, phi);
 }
 
-// K3: one CTA per group of 32 frontier points b (one k).  All points of an aligned
-// group share the same partial-chunk list, so the 128 threads (point o = tid/4,
-// block entry c = tid%4) sum the K2 partials with fully coalesced loads in a fixed
-// order; then each thread applies the predictor / corrector to its block entry.
-// The CTA holding b = n-1 also does the equal-time diagonal b = n.
-// Phi(t_{n-1/2}, k) comes from the per-step table (rebuilt per iteration for hf).
-__global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int phase, int it) {
+// K3: predictor / corrector / residual for the frontier points of ALL local k,
+// optionally fused with K1 (the Sigma slice of the updated frontier).
+//
+// One CTA owns PPC consecutive frontier points b for every local k; thread =
+// (k, point, block entry), so that a warp reads whole 64-byte blocks of PPC
+// consecutive points of one partial chunk (coalesced).  Phase A: each thread sums
+// the K2 partials of its block entry in chunk order (deterministic).  Phase B: it
+// applies Phi (G - i dt I) / (G + i dt I) Phi^dag (propagator.py:154-158,
+// 182-191).  The CTA holding b = n-1 also does the equal-time diagonal b = n
+// (propagator.py:193-212).  Phase C (SIGMA, one rank): the CTA now holds the new
+// G(t_n, t_b) of all k for its points (+ the diagonal), which is exactly what the
+// second-Born Sigma of those pairs needs, so it evaluates Sigma(n) there (K1's
+// math, selfenergy.py:59-325) instead of a separate launch.  That Sigma is the one
+// the next corrector iteration reads, and - for the last iteration - the Sigma(n)
+// that step n+1 starts from (propagator.py:331-333).
+// LANG = limit_mode (langreth): a template parameter so that the as-printed kernel
+// does not carry the langreth reductions' registers.
+// Points per CTA: up to 4 (and <= 512 threads), but small frontiers keep one point
+// per CTA so that the grid still spreads over the SMs.
+static int g_upd_min_ctas = -1;   // KBE_UPD_MIN_CTAS (tuning knob)
+static int upd_ppc(int nkl, int n) {
+    if (g_upd_min_ctas < 0) {
+        const char* e = getenv("KBE_UPD_MIN_CTAS");
+        g_upd_min_ctas = e ? atoi(e) : 148;
+    }
+    int p = 512 / (4 * nkl);
+    p = p < 1 ? 1 : (p > 4 ? 4 : p);
+    while (p > 1 && n / p < g_upd_min_ctas) p >>= 1;
+    return p;
+}
+static int upd_threads(int nkl, int ppc) { return ((ppc * 4 * nkl + 31) / 32) * 32; }
+static size_t upd_smem_bytes(int nkl, int nk, int ppc) {
+    return sizeof(cplx) * ((size_t)2 * ppc * nkl * 4          // sA, sB
+                           + (size_t)6 * nkl * 4              // sC, sRow, sCol, sX, sY, sZ
+                           + (size_t)2 * (ppc + 1) * 4 * nk   // V1, V2 (Sigma operands)
+                           + (size_t)(ppc + 1) * 16 * nk);    // P, X per component
+}
+
+template <int LANG, int SIGMA>
+__global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
         if (ctl->poisoned) return;
     } else if (kbe_skip(ctl, it, P.eps)) {
         return;
     }
-    const int kl = blockIdx.y;
-    const int nkl = P.k_hi - P.k_lo;
-    // thread = (point o, block entry c, chunk lane q): 8 x 4 x 4 = 128 threads; a CTA
-    // covers 8 points of one aligned group of 32 (all share one chunk list)
-    const int tid = threadIdx.x, q4 = tid & 3, c = (tid >> 2) & 3, o = tid >> 4;
-    const int grp = blockIdx.x >> 2, b0 = grp * 32 + (blockIdx.x & 3) * 8, b = b0 + o;
+    const int nkl = P.k_hi - P.k_lo, nk = P.n_k;
+    const int tid = threadIdx.x, T = blockDim.x;
+    const int b0 = blockIdx.x * PPC;
+    const int np = min(PPC, n - b0);           // own points b0 .. b0+np-1 (all < n)
     const int64_t N1 = P.n_steps + 1;
     const int nf = phase == 0 ? n - 1 : n;     // frontier of the collision being consumed
-    const bool diag_cta = b0 <= n - 1 && n - 1 < b0 + 8;
-    __shared__ cplx sA[8][4], sB[8][4], sC[4], sRow[4], sCol[4], sX[4], sY[4], sZ[4];
-    __shared__ double red[4];
-    __shared__ int redf[4];
-    if (phase == 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid < KBE_MAX_ITER) {
+    const bool diag_cta = b0 <= n - 1 && n - 1 < b0 + PPC;
+    const double dt = P.dt;
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    extern __shared__ cplx usm[];
+    cplx* sA = usm;                              // [PPC][nkl][4]  I<(t_nf, t_b)
+    cplx* sB = sA + PPC * nkl * 4;               // [PPC][nkl][4]  I>(t_b, t_nf)
+    cplx* sC = sB + PPC * nkl * 4;               // [nkl][4]       I<(t_n, t_n)
+    cplx* sRow = sC + nkl * 4;                   // [nkl][4]       new G<(n, n-1)
+    cplx* sCol = sRow + nkl * 4;                 // [nkl][4]       new G>(n-1, n)
+    cplx* sX = sCol + nkl * 4;                   // [nkl][4]       langreth extras
+    cplx* sY = sX + nkl * 4;
+    cplx* sZ = sY + nkl * 4;
+    cplx* V1 = sZ + nkl * 4;                     // [PPC+1][4][nk] G<(t_b, t_n)
+    cplx* V2 = V1 + (PPC + 1) * 4 * nk;          // [PPC+1][4][nk] G>(t_n, t_b)
+    cplx* PX = V2 + (PPC + 1) * 4 * nk;          // [PPC+1][2 comp][2 (P,X)][4][nk]
+    __shared__ double red[32];
+    __shared__ int redf[32];
+    if (phase == 0 && blockIdx.x == 0 && tid < KBE_MAX_ITER) {
         ctl->res[tid] = 0ull;
         ctl->nonfinite[tid] = 0;
     }
-    // ---- fixed-order partial sums: A = I<(t_nf, t_b), B = I>(t_b, t_nf); chunk lane q4
-    // sums chunks q4, q4+4, ... in order, then a fixed 2-level shuffle tree combines lanes.
-    {
-        const cplx* rowP = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
-        const cplx* colP = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
-        const cplx* gcP = (const cplx*)P.gc_part + ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
-        const cplx* gcC = P.limit_mode ? (const cplx*)P.gc_part_c + ((int64_t)kl * P.nsb * N1 + b) * 4 + c : nullptr;
-        const int64_t cs = N1 * 4;   // chunk stride
-        cplx a = cz(), g = cz();
-        if (b < n) {
-            const int nr = grp + 1, ns = nf / TS - grp + 1;
-#pragma unroll 4
-            for (int i = q4; i < nr + ns; i += 4)
-                a = cadd(a, i < nr ? rowP[i * cs] : colP[(grp + i - nr) * cs]);
-            if (b < nf) {
-                const int ng = gcC ? nr + ns : nr;   // langreth: + column-direction chunks
-#pragma unroll 4
-                for (int i = q4; i < ng; i += 4) g = cadd(g, i < nr ? gcP[i * cs] : gcC[(grp + i - nr) * cs]);
-            }
-        }
+    const int64_t cs = N1 * 4;   // partial chunk stride
+    const int cts = coll_ts(nf, nkl, LANG);
+    const int64_t plp = plane_len(n - 1), plc = plane_len(n);
+
+    // this thread's (k, point, entry)
+    const int c = tid & 3, o = (tid >> 2) % PPC, kl = (tid >> 2) / PPC;
+    const int b = b0 + o, i = c >> 1, j = c & 1;
+    const bool own = kl < nkl && o < np;
+    cplx* G = (cplx*)P.g_hist + (int64_t)(own ? kl : 0) * P.tri;
+    const cplx* prev = G + slice_off(n - 1);
+    cplx* cur = G + slice_off(n);
+    cplx* lro = (cplx*)P.lr_old + ((int64_t)(own ? kl : 0) * N1 + b) * 4;
+    cplx* clo = (cplx*)P.col_old + ((int64_t)(own ? kl : 0) * N1 + b) * 4;
+    const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + (own ? kl : 0)) * 4;
+
+    // operands that do not depend on the collision: issued first so that their
+    // latency overlaps the partial sums
+    cplx phr[2], phc[2], pgl[2], pgu[2], olr[2], ocl[2], ol = cz(), ou = cz();
 #pragma unroll
-        for (int off = 1; off <= 2; off <<= 1) {
-            a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
-            a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
-            g.x += __shfl_xor_sync(0xffffffffu, g.x, off);
-            g.y += __shfl_xor_sync(0xffffffffu, g.y, off);
-        }
-        if (q4 == 0) {
-            sA[o][c] = a;
-            sB[o][c] = g;
-        }
-        if (diag_cta && P.limit_mode && tid == 32) {
-            // langreth: I> rows and I< columns are independent of I< rows / I> columns
-            if (phase == 0) {
-                reduce_gr(P, kl, n - 1, n - 1, sX);   // greater_row_old[n-1]
-            } else {
-                reduce_lc(P, kl, n - 1, n, sX);       // lesser_col[n-1]
-                reduce_gr(P, kl, n - 1, n, sY);       // greater_row[n-1]
-                reduce_gr(P, kl, n, n, sZ);           // greater_row[n]
+    for (int k = 0; k < 2; ++k) {
+        phr[k] = phc[k] = pgl[k] = pgu[k] = olr[k] = ocl[k] = cz();
+        if (own) {
+            phr[k] = ph[i * 2 + k];
+            phc[k] = ph[j * 2 + k];
+            pgl[k] = prev[(k * 2 + j) * plp + b];
+            pgu[k] = prev[(4 + i * 2 + k) * plp + b];
+            if (phase == 1) {
+                olr[k] = lro[k * 2 + j];
+                ocl[k] = clo[i * 2 + k];
             }
         }
-        if (phase == 1 && diag_cta && tid < 4) {   // C = I<(t_n, t_n)
-            const int cc = tid;
-            const cplx* rp = (const cplx*)P.row_part + ((int64_t)kl * P.nbb * N1 + n) * 4 + cc;
-            const cplx* cp = (const cplx*)P.col_part + ((int64_t)kl * P.nsb * N1 + n) * 4 + cc;
+    }
+    if (own && phase == 1) {
+        ol = cur[c * plc + b];
+        ou = cur[(4 + c) * plc + b];
+    }
+
+    // ---- phase A: fixed-order partial sums -------------------------------------------
+    if (own) {
+        // row chunks bc = 0 .. b/TB, then column chunks b/ts .. nf/ts (langreth: ts = TB)
+        const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;   // [k][chunk][point][4]
+        const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
+        const cplx* rowP = (const cplx*)P.row_part + rb;
+        const cplx* colP = (const cplx*)P.col_part + cb;
+        const cplx* gcP = (const cplx*)P.gc_part + rb;
+        const cplx* gcC = LANG ? (const cplx*)P.gc_part_c + cb : nullptr;
+        const int c0 = b / cts;
+        const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
+        const int na = nr + ns, ng = b < nf ? (LANG ? nr + ns : nr) : 0;
+        cplx a = cz(), g = cz();
+        for (int i0 = 0; i0 < na || i0 < ng; i0 += 4) {
+            cplx va[4], vg[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = i0 + u;
+                va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
+                vg[u] = q < ng ? (q < nr ? gcP[q * cs] : gcC[(c0 + q - nr) * cs]) : cz();
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (i0 + u < na) a = cadd(a, va[u]);
+                if (i0 + u < ng) g = cadd(g, vg[u]);
+            }
+        }
+        sA[(o * nkl + kl) * 4 + c] = a;
+        sB[(o * nkl + kl) * 4 + c] = g;
+    }
+    if (diag_cta) {
+        if (LANG) {
+            // langreth: I> rows and I< columns are independent of I< rows / I> columns
+            for (int k2 = tid; k2 < nkl; k2 += T) {
+                if (phase == 0) {
+                    reduce_gr(P, k2, n - 1, n - 1, sX + k2 * 4);   // greater_row_old[n-1]
+                } else {
+                    reduce_lc(P, k2, n - 1, n, sX + k2 * 4);       // lesser_col[n-1]
+                    reduce_gr(P, k2, n - 1, n, sY + k2 * 4);       // greater_row[n-1]
+                    reduce_gr(P, k2, n, n, sZ + k2 * 4);           // greater_row[n]
+                }
+            }
+        }
+        if (phase == 1) {
+            // C = I<(t_n, t_n): thread = (k, entry cc, chunk lane q), PPC lanes per entry
+            // (consecutive lanes: fixed xor-shuffle tree), one round over the CTA
+            const int L = PPC;
+            const int nrc = n / TB + 1;   // row chunks, then the one column chunk holding n
+            const int cn = n / coll_ts(n, nkl, LANG);
+            const int q = tid % L, cc = (tid / L) & 3, k2 = tid / (4 * L);
             cplx x = cz();
-            for (int bc = 0; bc <= n / TB; ++bc) x = cadd(x, rp[bc * cs]);
-            x = cadd(x, cp[(n / TS) * cs]);
-            sC[cc] = x;
+            if (k2 < nkl) {
+                const cplx* rp = (const cplx*)P.row_part + (((int64_t)k2 * P.nbb * N1 + n) * 4 + cc);
+                const cplx* cp = (const cplx*)P.col_part + (((int64_t)k2 * P.nsb * N1 + n) * 4 + cc);
+                for (int i0 = q; i0 <= nrc; i0 += 4 * L) {
+                    cplx v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int qq = i0 + L * u;
+                        v[u] = qq < nrc ? rp[qq * cs] : (qq == nrc ? cp[cn * cs] : cz());
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (i0 + L * u <= nrc) x = cadd(x, v[u]);
+                }
+            }
+            for (int off = 1; off < L; off <<= 1) {
+                x.x += __shfl_xor_sync(0xffffffffu, x.x, off);
+                x.y += __shfl_xor_sync(0xffffffffu, x.y, off);
+            }
+            if (k2 < nkl && q == 0) sC[k2 * 4 + cc] = x;
         }
     }
     __syncthreads();
-    cplx phi[4];
-    {
-        const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) phi[q] = ph[q];
-    }
-    const double dt = P.dt;
-    cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
-    const cplx* prev = G + slice_off(n - 1);
-    const int64_t plp = plane_len(n - 1);
-    cplx* cur = G + slice_off(n);
-    const int64_t plc = plane_len(n);
-    cplx* lro = (cplx*)P.lr_old + ((int64_t)kl * N1) * 4;
-    cplx* clo = (cplx*)P.col_old + ((int64_t)kl * N1) * 4;
-    cplx* fs = nullptr;
-    int64_t pm = 0;
-    if (P.front_send) {
-        pm = plane_len(P.n_steps);
-        fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-    }
-    const int i = c >> 1, j = c & 1;
+
+    // ---- phase B: row / column update of the own points ----------------------------------
+    const int64_t pm = P.front_send ? plane_len(P.n_steps) : 0;
     double res = 0.0;
     bool fin = true;
-    if (b < n && q4 == 0) {
-        // irow / icol: the collision blocks entering the row and column updates
-        auto IR = [&](int q) -> cplx {
-            return phase == 0 ? sA[o][q] : cscale(cadd(lro[b * 4 + q], sA[o][q]), 0.5);
-        };
-        auto IC = [&](int q) -> cplx {
-            if (phase == 0) {
-                if (b < n - 1) return sB[o][q];
-                return P.limit_mode ? sX[q] : cneg(sA[o][q]);   // greater_row[n-1] (= -lesser_row, as-printed)
-            }
-            return cscale(cadd(clo[b * 4 + q], sB[o][q]), 0.5);
+    if (own) {
+        const cplx* A = sA + (o * nkl + kl) * 4;
+        const cplx* B = sB + (o * nkl + kl) * 4;
+        // predictor column input: I>(t_b, t_{n-1}); b = n-1 takes greater_row[n-1]
+        // (= -lesser_row as printed; the langreth reduction otherwise)
+        auto IC0 = [&](int q) -> cplx {
+            if (b < n - 1) return B[q];
+            return LANG ? sX[kl * 4 + q] : cneg(A[q]);
         };
         if (phase == 0) {
-            lro[b * 4 + c] = IR(c);
-            clo[b * 4 + c] = IC(c);
+            lro[c] = A[c];
+            clo[c] = IC0(c);
         }
         // row(i,j) = sum_k Phi(i,k) [G<(n-1,b)(k,j) - i dt ir(k,j)]
         // col(i,j) = sum_k [G>(b,n-1)(i,k) + i dt ic(i,k)] conj(Phi(j,k))
-        const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
         cplx row = cz(), col = cz();
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const cplx gl = prev[(k * 2 + j) * plp + b];
-            row = cfma(ph[i * 2 + k], csub(gl, cmul_pi(IR(k * 2 + j), dt)), row);
-            const cplx gu = prev[(4 + i * 2 + k) * plp + b];
-            col = cfma_cb(cadd(gu, cmul_pi(IC(i * 2 + k), dt)), ph[j * 2 + k], col);
+            const cplx ir = phase == 0 ? A[k * 2 + j] : cscale(cadd(olr[k], A[k * 2 + j]), 0.5);
+            const cplx ic = phase == 0 ? IC0(i * 2 + k) : cscale(cadd(ocl[k], B[i * 2 + k]), 0.5);
+            row = cfma(phr[k], csub(pgl[k], cmul_pi(ir, dt)), row);
+            col = cfma_cb(cadd(pgu[k], cmul_pi(ic, dt)), phc[k], col);
         }
         if (phase == 1) {
-            const cplx ol = cur[c * plc + b], ou = cur[(4 + c) * plc + b];
-            res = fmax(hypot(row.x - ol.x, row.y - ol.y), hypot(col.x - ou.x, col.y - ou.y));
-            if (res != res) res = __longlong_as_double(0x7ff8000000000000LL);
-            fin = isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
-            if (b == n - 1) { sRow[c] = row; sCol[c] = col; }
+            const double d1 = hypot(row.x - ol.x, row.y - ol.y), d2 = hypot(col.x - ou.x, col.y - ou.y);
+            res = (d1 != d1 || res != res) ? nan : fmax(res, d1);
+            res = (d2 != d2 || res != res) ? nan : fmax(res, d2);
+            fin = fin && isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
         }
+        if (b == n - 1) { sRow[kl * 4 + c] = row; sCol[kl * 4 + c] = col; }
         cur[c * plc + b] = row;
         cur[(4 + c) * plc + b] = col;
-        if (fs) { fs[c * pm + b] = row; fs[(4 + c) * pm + b] = col; }
+        if (P.front_send) {
+            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
+            fs[c * pm + b] = row;
+            fs[(4 + c) * pm + b] = col;
+        }
+        if (SIGMA) {   // Sigma operands of pair b: G<(t_b,t_n) = -row^dag, G>(t_n,t_b) = -col^dag
+            const int t = (c & 1) * 2 + (c >> 1);
+            V1[(o * 4 + t) * nk + P.k_lo + kl] = cneg(cconj(row));
+            V2[(o * 4 + t) * nk + P.k_lo + kl] = cneg(cconj(col));
+        }
     }
     if (diag_cta) {
-        if (phase == 1) __syncthreads();   // sRow / sCol of point n-1
-        if (tid == 0) {
-            cplx nl[4], nu[4];
+        __syncthreads();   // sRow / sCol of point n-1
+        for (int item = tid; item < nkl * 4; item += T) {
+            // equal-time diagonal b = n, one block entry (j, m) per item; each item also
+            // forms the transposed entry it needs for the anti-Hermitian part.  Same
+            // operation order as the 2x2 helpers.
+            const int e = item & 3, kl = item >> 2;
+            const int dj = e >> 1, dm = e & 1;
+            cplx* G = (cplx*)P.g_hist + (int64_t)kl * P.tri;
+            const cplx* prev = G + slice_off(n - 1);
+            cplx* cur = G + slice_off(n);
+            const cplx* ph = (const cplx*)P.phi + ((int64_t)n * nkl + kl) * 4;
+            auto PH = [&](int r, int c2) -> cplx { return ph[r * 2 + c2]; };
+            auto sandwich = [&](const cplx* X, int r, int q) -> cplx {   // (Phi X Phi^dag)(r, q)
+                cplx t0 = cfma(PH(r, 1), X[2], cfma(PH(r, 0), X[0], cz()));
+                cplx t1 = cfma(PH(r, 1), X[3], cfma(PH(r, 0), X[1], cz()));
+                return cfma_cb(t1, PH(q, 1), cfma_cb(t0, PH(q, 0), cz()));
+            };
+            auto ah = [](cplx x, cplx y) -> cplx {   // (x - conj(y)) / 2
+                return make_double2(0.5 * (x.x - y.x), 0.5 * (x.y + y.y));
+            };
+            cplx nl, nu;
             if (phase == 0) {
-                cplx gl[4], gu[4], tt[4], d[4];
+                cplx gl[4], gu[4];
                 load_cell(prev, plp, n - 1, gl, gu);
-                mm(tt, phi, gl);
-                mm_bdag(d, tt, phi);
-                antiherm(nl, d);
-                mm(tt, phi, gu);
-                mm_bdag(d, tt, phi);
-                antiherm(nu, d);
+                nl = ah(sandwich(gl, dj, dm), sandwich(gl, dm, dj));
+                nu = ah(sandwich(gu, dj, dm), sandwich(gu, dm, dj));
             } else {
-                cplx row[4], col[4], ml[4], mg[4], src[4], d[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) { row[q] = sRow[q]; col[q] = sCol[q]; }
-                neg_dag(ml, row);   // mirror of the fresh row entry (propagator.py:193)
-                neg_dag(mg, col);
                 const int o1 = (n - 1) - b0;
-                // i_dl = (lesser_col[n-1] + lesser_row[n]) / 2, lesser_col = -greater_col
-                // i_dg = (greater_row[n-1] + greater_row[n]) / 2, greater_row = -lesser_row
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const cplx lc1 = P.limit_mode ? sX[q] : cneg(sB[o1][q]);
-                    const cplx idl = cscale(cadd(lc1, sC[q]), 0.5);
-                    src[q] = csub(ml[q], cmul_pi(idl, dt));
-                }
-                mm(d, phi, src);
-                antiherm(nl, d);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const cplx gr1 = P.limit_mode ? sY[q] : cneg(sA[o1][q]);
-                    const cplx gr2 = P.limit_mode ? sZ[q] : cneg(sC[q]);
-                    const cplx idg = cscale(cadd(gr1, gr2), 0.5);
-                    src[q] = cadd(mg[q], cmul_pi(idg, dt));
-                }
-                mm_bdag(d, src, phi);
-                antiherm(nu, d);
-                cplx ol[4], ou[4];
-                load_cell(cur, plc, n, ol, ou);
-                res = absmax4(nl, ol, res);
-                res = absmax4(nu, ou, res);
-                fin = fin && finite4(nl) && finite4(nu);
+                const cplx* A1 = sA + (o1 * nkl + kl) * 4;
+                const cplx* B1 = sB + (o1 * nkl + kl) * 4;
+                const cplx* C = sC + kl * 4;
+                // src_l = mirror(row) - i dt (lesser_col[n-1] + lesser_row[n]) / 2
+                auto srcl = [&](int r, int q) -> cplx {
+                    const cplx ml = cneg(cconj(sRow[kl * 4 + q * 2 + r]));
+                    const cplx lc1 = LANG ? sX[kl * 4 + r * 2 + q] : cneg(B1[r * 2 + q]);
+                    return csub(ml, cmul_pi(cscale(cadd(lc1, C[r * 2 + q]), 0.5), dt));
+                };
+                // src_g = mirror(col) + i dt (greater_row[n-1] + greater_row[n]) / 2
+                auto srcg = [&](int r, int q) -> cplx {
+                    const cplx mg = cneg(cconj(sCol[kl * 4 + q * 2 + r]));
+                    const cplx gr1 = LANG ? sY[kl * 4 + r * 2 + q] : cneg(A1[r * 2 + q]);
+                    const cplx gr2 = LANG ? sZ[kl * 4 + r * 2 + q] : cneg(C[r * 2 + q]);
+                    return cadd(mg, cmul_pi(cscale(cadd(gr1, gr2), 0.5), dt));
+                };
+                auto dl = [&](int r, int q) -> cplx {   // (Phi src_l)(r, q)
+                    return cfma(PH(r, 1), srcl(1, q), cfma(PH(r, 0), srcl(0, q), cz()));
+                };
+                auto dg = [&](int r, int q) -> cplx {   // (src_g Phi^dag)(r, q)
+                    return cfma_cb(srcg(r, 1), PH(q, 1), cfma_cb(srcg(r, 0), PH(q, 0), cz()));
+                };
+                nl = ah(dl(dj, dm), dl(dm, dj));
+                nu = ah(dg(dj, dm), dg(dm, dj));
+                const cplx ol = cur[e * plc + n], ou = cur[(4 + e) * plc + n];
+                const double d1 = hypot(nl.x - ol.x, nl.y - ol.y), d2 = hypot(nu.x - ou.x, nu.y - ou.y);
+                res = (d1 != d1 || res != res) ? nan : fmax(res, d1);
+                res = (d2 != d2 || res != res) ? nan : fmax(res, d2);
+                fin = fin && isfinite(nl.x) && isfinite(nl.y) && isfinite(nu.x) && isfinite(nu.y);
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                cur[q * plc + n] = nl[q];
-                cur[(4 + q) * plc + n] = nu[q];
-                if (fs) { fs[q * pm + n] = nl[q]; fs[(4 + q) * pm + n] = nu[q]; }
+            cur[e * plc + n] = nl;
+            cur[(4 + e) * plc + n] = nu;
+            if (P.front_send) {
+                cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
+                fs[e * pm + n] = nl;
+                fs[(4 + e) * pm + n] = nu;
+            }
+            if (SIGMA) {   // pair n: G<(t_n,t_n), G>(t_n,t_n) as stored
+                V1[(PPC * 4 + e) * nk + P.k_lo + kl] = nl;
+                V2[(PPC * 4 + e) * nk + P.k_lo + kl] = nu;
             }
         }
     }
     if (phase == 1) {
-        const int lane = tid & 31, warp = tid >> 5;
+        const int lane = tid & 31, warp = tid >> 5, nw = (T + 31) >> 5;
         for (int off = 16; off > 0; off >>= 1) {
             const double other = __shfl_xor_sync(0xffffffffu, res, off);
-            res = (res != res || other != other) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(res, other);
+            res = (res != res || other != other) ? nan : fmax(res, other);
         }
         const unsigned ballot = __ballot_sync(0xffffffffu, !fin);
         if (lane == 0) { red[warp] = res; redf[warp] = ballot != 0; }
@@ -1213,8 +1390,8 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
         if (tid == 0) {
             double r = red[0];
             int nfl = redf[0];
-            for (int w = 1; w < 4; ++w) {
-                r = (r != r || red[w] != red[w]) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(r, red[w]);
+            for (int w = 1; w < nw; ++w) {
+                r = (r != r || red[w] != red[w]) ? nan : fmax(r, red[w]);
                 nfl |= redf[w];
             }
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
@@ -1222,10 +1399,68 @@ __global__ void __launch_bounds__(128) update_kernel(kbe_problem P, int n, int p
             if (nfl) atomicOr(&ctl->nonfinite[it], 1);
         }
     }
+
+    // ---- phase C: Sigma(n) of the CTA's pairs (own points + the diagonal) ----------------
+    if (SIGMA) {
+        __syncthreads();
+        const int nslot = PPC + 1;
+        auto slot_b = [&](int p) -> int { return p < PPC ? (p < np ? b0 + p : -1) : (diag_cta ? n : -1); };
+        const int64_t pmf = plane_len(P.n_steps);
+        if (phase == 0 && P.s_fresh && n >= 2) {
+            // predictor of step n: the fresh Sigma(n-1) the step started from (consumed by
+            // collision(n-1)) is the reference's Sigma slice n-1 (propagator.py:331-333).
+            // The CTAs' own points 0..n-1 cover the whole slice.  (Stage 2 rewrites
+            // s_fresh only after the barrier below.)
+            cplx* hp = (cplx*)P.s_hist + slice_off(n - 1);
+            const int64_t plq = plane_len(n - 1);
+            for (int item = tid; item < np * 8 * nkl; item += T) {
+                const int kl = item % nkl, plane = (item / nkl) & 7, b = b0 + item / (8 * nkl);
+                hp[(int64_t)kl * P.tri + plane * plq + b] = ((const cplx*)P.s_fresh)[((int64_t)kl * 8 + plane) * pmf + b];
+            }
+        }
+        // stage 1: P and X, one (pair, component, jm, q) per item
+        for (int item = tid; item < nslot * 8 * nk; item += T) {
+            const int q = item % nk, jm = (item / nk) & 3, comp = (item / (4 * nk)) & 1, p = item / (8 * nk);
+            if (slot_b(p) < 0) continue;
+            const cplx* gp = (comp == 0 ? V1 : V2) + p * 4 * nk;
+            const cplx* gr = (comp == 0 ? V2 : V1) + p * 4 * nk;
+            cplx* base = PX + (p * 2 + comp) * 8 * nk;
+            base[jm * nk + q] = sig_pol(gp, gr, nk, jm, q);
+            base[4 * nk + jm * nk + q] = sig_x(gp, gr, nk, jm, q);
+        }
+        __syncthreads();
+        // stage 2: Sigma1 - Sigma2 on the local k, written to Sigma slice n
+        cplx* dst0 = (cplx*)P.s_hist + slice_off(n);
+
+        for (int item = tid; item < nslot * 8 * nkl; item += T) {
+            const int kl = item % nkl, jm = (item / nkl) & 3, comp = (item / (4 * nkl)) & 1, p = item / (8 * nkl);
+            const int b = slot_b(p);
+            if (b < 0) continue;
+            const cplx* gp = (comp == 0 ? V1 : V2) + p * 4 * nk;
+            const cplx* base = PX + (p * 2 + comp) * 8 * nk;
+            const int k = P.k_lo + kl;
+            const double pref = (P.u_table[b] * P.u_table[n]) / ((double)nk * (double)nk);
+            const cplx s1 = cscale(sig_s1(base, gp, nk, jm, k), pref);
+            const cplx s2 = cscale(sig_s2(gp, base + 4 * nk, nk, jm, k), pref);
+            const int plane = comp == 0 ? 4 + jm : jm;
+            const cplx v = csub(s1, s2);
+            if (P.s_fresh) {
+                // the Sigma the collision just consumed becomes the history's slice
+                // (reference state: Sigma(n) of the last evaluated iterate); the new
+                // one waits in s_fresh for the next collision
+                cplx* f = (cplx*)P.s_fresh + ((int64_t)kl * 8 + plane) * pmf + b;
+                if (phase == 1) dst0[(int64_t)kl * P.tri + plane * plc + b] = *f;
+                *f = v;
+            } else {
+                dst0[(int64_t)kl * P.tri + plane * plc + b] = v;
+            }
+        }
+    }
 }
 
 // Phi(t_{n-1/2}, k) for steps n in [n0, n1], local k (hf term from ctl->hf_sum when hf_mode="on")
 __global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int check_skip) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (check_skip && kbe_skip(ctl, it, P.eps)) return;
     const int nkl = P.k_hi - P.k_lo;
@@ -1242,6 +1477,7 @@ __global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int chec
 
 // hf_mode="on": k-sum of rho(t_{n-1}) (phase 0) or of (rho(t_{n-1}) + rho(t_n))/2 (phase 1)
 __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(ctl, it, P.eps)) return;
     const int nloc = P.k_hi - P.k_lo;
@@ -1276,6 +1512,7 @@ __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
 
 // =================================================================== K4: finish
 __global__ void finish_kernel(kbe_problem P, int n) {
+    pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (ctl->poisoned) return;
     const int nloc = P.k_hi - P.k_lo;
@@ -1317,6 +1554,7 @@ __global__ void finish_kernel(kbe_problem P, int n) {
 
 // =================================================================== init / pack / unpack
 __global__ void init_slice0_kernel(kbe_problem P) {
+    pdl_enter();
     const int kl = blockIdx.x * blockDim.x + threadIdx.x;
     if (kl < P.k_hi - P.k_lo) {
         cplx* g = (cplx*)P.g_hist + (int64_t)kl * P.tri;   // slice 0: plane_len(0) = 8
@@ -1385,6 +1623,32 @@ __global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int 
 }
 
 // =================================================================== host side
+// Launch with programmatic stream serialization (see pdl_enter); KBE_NO_PDL=1
+// falls back to plain stream order (for A/B timing).
+static int g_pdl = -1;
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, void* stream, Args&&... args) {
+    if (g_pdl < 0) {
+        const char* e = getenv("KBE_NO_PDL");
+        g_pdl = (e && e[0] == '1') ? 0 : 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#define KBE_LAUNCH(name, ...)                                              \
+    do {                                                                   \
+        cudaError_t e_ = launch(__VA_ARGS__);                              \
+        if (e_ != cudaSuccess) { set_err(name, e_); return KBE_ERR_CUDA; } \
+    } while (0)
 static bool g_attr_done = false;
 static int g_num_sms = 148;
 static int g_coll_occ = 8;   // resident collision CTAs per SM (occupancy API)
@@ -1406,6 +1670,14 @@ static int ensure_attrs() {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, collision_kernel, 32, sizeof(CollSmem));
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
+    {
+        void (*upd[4])(kbe_problem, int, int, int, int) = {update_kernel<0, 0>, update_kernel<0, 1>, update_kernel<1, 0>,
+                                                      update_kernel<1, 1>};
+        for (int i = 0; i < 4; ++i) {
+            e = cudaFuncSetAttribute(upd[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(update)", e); return KBE_ERR_CUDA; }
+        }
+    }
     e = cudaFuncSetAttribute(sigma_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_slice)", e); return KBE_ERR_CUDA; }
     g_attr_done = true;
@@ -1430,6 +1702,22 @@ static int check_problem(const kbe_problem* p) {
     return KBE_OK;
 }
 
+static int launch_update(const kbe_problem* p, int n, int phase, int it, int sigma, void* stream) {
+    int rc = ensure_attrs();
+    if (rc) return rc;
+    const int nkl = p->k_hi - p->k_lo, ppc = upd_ppc(nkl, n);
+    const dim3 grid((n + ppc - 1) / ppc), block(upd_threads(nkl, ppc));
+    const size_t smem = upd_smem_bytes(nkl, p->n_k, ppc);
+    if (p->limit_mode) {
+        if (sigma) KBE_LAUNCH("update_kernel", update_kernel<1, 1>, grid, block, smem, stream, *p, n, phase, it, ppc);
+        else KBE_LAUNCH("update_kernel", update_kernel<1, 0>, grid, block, smem, stream, *p, n, phase, it, ppc);
+    } else {
+        if (sigma) KBE_LAUNCH("update_kernel", update_kernel<0, 1>, grid, block, smem, stream, *p, n, phase, it, ppc);
+        else KBE_LAUNCH("update_kernel", update_kernel<0, 0>, grid, block, smem, stream, *p, n, phase, it, ppc);
+    }
+    return KBE_OK;
+}
+
 extern "C" {
 
 int kbe_abi_version(void) { return KBE_ABI_VERSION; }
@@ -1449,11 +1737,10 @@ int kbe_init_history(const kbe_problem* p, void* stream) {
     if (e == cudaSuccess) e = cudaMemsetAsync(p->s_hist, 0, bytes, st);
     if (e != cudaSuccess) { set_err("cudaMemsetAsync(history)", e); return KBE_ERR_CUDA; }
     const int nloc = p->k_hi - p->k_lo;
-    init_slice0_kernel<<<(nloc + 127) / 128, 128, 0, st>>>(*p);
-    KBE_CHECK_LAUNCH("init_slice0_kernel");
+    KBE_LAUNCH("init_slice0_kernel", init_slice0_kernel, dim3((nloc + 127) / 128), dim3(128), 0, st, *p);
     const int64_t cnt = (int64_t)p->n_steps * nloc;
-    phi_table_kernel<<<(int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096), 256, 0, st>>>(*p, 1, p->n_steps, 0, 0);
-    KBE_CHECK_LAUNCH("phi_table_kernel");
+    KBE_LAUNCH("phi_table_kernel", phi_table_kernel, dim3((int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096)),
+               dim3(256), 0, st, *p, 1, p->n_steps, 0, 0);
     return KBE_OK;
 }
 
@@ -1468,8 +1755,8 @@ int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream
     if ((rc = ensure_attrs())) return rc;
     const int pb = sigma_pairs_per_block(p->n_k);
     const int grid = (n + 1 + pb - 1) / pb;
-    sigma_frontier_kernel<<<grid, sigma_threads(p->n_k), sigma_smem_bytes(p->n_k, pb), (cudaStream_t)stream>>>(*p, n, it);
-    KBE_CHECK_LAUNCH("sigma_frontier_kernel");
+    KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel, dim3(grid), dim3(sigma_threads(p->n_k)),
+               sigma_smem_bytes(p->n_k, pb), stream, *p, (int)n, (int)it);
     return KBE_OK;
 }
 
@@ -1497,19 +1784,21 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
-    const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
-    const int64_t total = (int64_t)(T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * (p->k_hi - p->k_lo);
+    const int nkl = p->k_hi - p->k_lo;
+    const int64_t total = (int64_t)coll_tiles(n, nkl) * (TS / coll_ts(n, nkl, 0));
     const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
     const int grid = (int)(total < cap ? total : cap);
     if (p->limit_mode)
     {
+        const int T0 = n / TS + 1;
         const int64_t tl = 2 * (int64_t)(T0 * (T0 + 1) / 2) * (p->k_hi - p->k_lo);
         const int64_t cl = (int64_t)g_num_sms * g_lang_occ;
-        collision_langreth_kernel<<<(int)(tl < cl ? tl : cl), 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
+        KBE_LAUNCH("collision_langreth_kernel", collision_langreth_kernel, dim3((int)(tl < cl ? tl : cl)), dim3(32),
+                   sizeof(CollSmem), stream, *p, (int)n, (int)it);
+    } else {
+        KBE_LAUNCH("collision_kernel", collision_kernel, dim3(grid), dim3(32), sizeof(CollSmem), stream, *p, (int)n,
+                   (int)it);
     }
-    else
-        collision_kernel<<<grid, 32, sizeof(CollSmem), (cudaStream_t)stream>>>(*p, n, it);
-    KBE_CHECK_LAUNCH("collision_kernel");
     return KBE_OK;
 }
 
@@ -1518,9 +1807,8 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
     int rc = check_problem(p);
     if (rc) return rc;
     dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
-    collision_slice_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, (cplx*)lesser_row, (cplx*)greater_row,
-                                                                   (cplx*)lesser_col, (cplx*)greater_col);
-    KBE_CHECK_LAUNCH("collision_slice_kernel");
+    KBE_LAUNCH("collision_slice_kernel", collision_slice_kernel, grid, dim3(128), 0, stream, *p, (int)n,
+               (cplx*)lesser_row, (cplx*)greater_row, (cplx*)lesser_col, (cplx*)greater_col);
     return KBE_OK;
 }
 
@@ -1528,17 +1816,24 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    dim3 grid((n + 7) / 8, p->k_hi - p->k_lo);
-    update_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
-    KBE_CHECK_LAUNCH("update_kernel");
-    return KBE_OK;
+    return launch_update(p, n, phase, it, 0, stream);
+}
+
+int kbe_update_sigma(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update_sigma: n/it", cudaSuccess); return KBE_ERR_ARG; }
+    if (p->k_lo != 0 || p->k_hi != p->n_k || p->front_all) {
+        snprintf(g_err, sizeof(g_err), "kbe_update_sigma: the fused Sigma needs all k on one rank");
+        return KBE_ERR_ARG;
+    }
+    return launch_update(p, n, phase, it, p->interacting ? 1 : 0, stream);
 }
 
 int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    hf_mean_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(*p, n, phase, it);
-    KBE_CHECK_LAUNCH("hf_mean_kernel");
+    KBE_LAUNCH("hf_mean_kernel", hf_mean_kernel, dim3(1), dim3(128), 0, stream, *p, (int)n, (int)phase, (int)it);
     return KBE_OK;
 }
 
@@ -1546,16 +1841,14 @@ int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps) { set_err("kbe_build_phi: n", cudaSuccess); return KBE_ERR_ARG; }
-    phi_table_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(*p, n, n, it, 1);
-    KBE_CHECK_LAUNCH("phi_table_kernel");
+    KBE_LAUNCH("phi_table_kernel", phi_table_kernel, dim3(1), dim3(128), 0, stream, *p, (int)n, (int)n, (int)it, 1);
     return KBE_OK;
 }
 
 int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    finish_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(*p, n);
-    KBE_CHECK_LAUNCH("finish_kernel");
+    KBE_LAUNCH("finish_kernel", finish_kernel, dim3(1), dim3(256), 0, stream, *p, (int)n);
     return KBE_OK;
 }
 
@@ -1567,16 +1860,17 @@ int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
         return KBE_ERR_ARG;
     }
     if (n < 1 || n > p->n_steps) { set_err("kbe_step: n", cudaSuccess); return KBE_ERR_ARG; }
+    // Sigma(n-1) was produced by the last update of step n-1 (fused, see update_kernel);
+    // only the ground state's Sigma(0) needs the standalone K1.
     const int nold = n - 1;
-    if (p->interacting && (rc = kbe_sigma_frontier(p, nold, 0, stream))) return rc;
+    if (nold == 0 && p->interacting && (rc = kbe_sigma_frontier(p, 0, 0, stream))) return rc;
     if ((rc = kbe_collision_frontier(p, nold, 0, stream))) return rc;
     if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
-    if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
+    if ((rc = kbe_update_sigma(p, n, 0, 0, stream))) return rc;
     for (int it = 0; it < p->max_iter; ++it) {
-        if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
         if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
         if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
-        if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
+        if ((rc = kbe_update_sigma(p, n, 1, it, stream))) return rc;
     }
     return kbe_finish_step(p, n, stream);
 }
