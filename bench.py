@@ -34,8 +34,46 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "KBE time-steps/sec (whole propagation)"
-CFG = dict(n_k=16, n_steps=1000, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5)
-WORKLOAD = "cfg2: 1D Hubbard chain n_k=16, second-Born, 1000 time steps"
+# BASELINE.json configs; cfg2 (configs[1]) is the headline line, the others are
+# selectable with --workload for the per-config evidence under profiles/.
+# U is lowered where the reference's own as-printed scheme diverges.
+WORKLOADS = {
+    "cfg1": dict(n_k=2, n_steps=200, dt=0.02, u=1.0, pulse_intensity=0.2, pulse_center=0.5,
+                 workload="cfg1: Hubbard dimer n_k=2, second-Born, 200 time steps"),
+    "cfg2": dict(n_k=16, n_steps=1000, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5,
+                 workload="cfg2: 1D Hubbard chain n_k=16, second-Born, 1000 time steps"),
+    "cfg3": dict(n_k=64, n_steps=1000, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5, synth=True,
+                 workload="cfg3: synthetic dense-interaction n_k=64 (seeded band/U tables), 1000 time steps"),
+    "cfg4": dict(n_k=32, n_steps=4000, dt=0.02, u=0.25, pulse_intensity=0.2, pulse_center=0.5,
+                 workload="cfg4: long-time n_k=32, 4000 time steps (history-streaming)"),
+    "cfg5": dict(n_k=128, n_steps=500, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5,
+                 workload="cfg5: large basis n_k=128, 500 time steps"),
+}
+CFG = dict(WORKLOADS["cfg2"])
+WORKLOAD = CFG["workload"]
+
+
+def select_workload(name):
+    global CFG, WORKLOAD
+    CFG = dict(WORKLOADS[name])
+    WORKLOAD = CFG["workload"]
+    return CFG
+
+
+def model_kwargs(cfg=None):
+    """ModelConfig kwargs of a workload.  cfg3's synthetic system:
+    seeded tabulated bands eps_c = 1 + U(0,1), eps_v = -eps_c and a seeded U(t)
+    table u*(1 + 0.1 N(0,1)), all from default_rng(7)."""
+    c = cfg if cfg is not None else CFG
+    kw = dict(pulse_intensity=c["pulse_intensity"], pulse_center=c["pulse_center"])
+    if c.get("synth"):
+        rng = np.random.default_rng(7)
+        eps_c = 1.0 + rng.uniform(0.0, 1.0, c["n_k"])
+        kw.update(u_protocol=c["u"] * (1.0 + 0.1 * rng.standard_normal(c["n_steps"] + 1)),
+                  eps_c_table=eps_c, eps_v_table=-eps_c)
+    else:
+        kw.update(u_protocol=c["u"])
+    return kw
 
 
 def _peaks():
@@ -95,7 +133,7 @@ def cpu_baseline(iterations_per_step=None, budget_s=25.0):
     GPU run's iteration counts (1 + it_n evaluations at step n)."""
     from oracle import kbe_oracle as O
     n_k, N, dt = CFG["n_k"], CFG["n_steps"], CFG["dt"]
-    ns = [100, 200, 300]
+    ns = {2: [100, 200, 300], 16: [100, 200, 300], 32: [50, 100, 150], 64: [20, 40, 60]}.get(n_k, [8, 16, 24])
     cap = max(ns)
     drv = O.OracleDriver(n_k, O.Model(u_protocol=1.0), dt, cap)
     GL, GG = O.random_mirrored_state(n_k, cap, cap, seed=3)
@@ -132,8 +170,8 @@ def cpu_baseline(iterations_per_step=None, budget_s=25.0):
     return {
         "value": N / total, "unit": "time-steps/s", "cores": 1, "kind": "port",
         "sample": (f"numpy oracle port, single Sigma+collision evaluations at n={ns[:m]} on a random "
-                   f"n_k=16 history ({time.perf_counter() - t_all:.1f}s of CPU), fitted and extrapolated "
-                   f"to the full 1000-step propagation with the measured iteration counts"),
+                   f"n_k={n_k} history ({time.perf_counter() - t_all:.1f}s of CPU), fitted and extrapolated "
+                   f"to the full {N}-step propagation with the measured iteration counts"),
         "extrapolated_seconds": total,
     }
 
@@ -170,8 +208,7 @@ def _max_over_ranks(x, world):
 
 
 def _make_driver(kb):
-    model = kb.ModelConfig(u_protocol=CFG["u"], pulse_intensity=CFG["pulse_intensity"],
-                           pulse_center=CFG["pulse_center"])
+    model = kb.ModelConfig(**model_kwargs())
     cfg = kb.StepConfig(dt=CFG["dt"], n_steps=CFG["n_steps"], memory_budget=1 << 40)
     return model, cfg
 
@@ -206,19 +243,16 @@ def _collision_roofline(kb, drv, hbm_peak):
         calls = [(n - 1, 0)] + [(n, it) for it in range(drv.cfg.max_iter)]
         if drv.world > 1:
             raise RuntimeError("roofline pass runs on one rank")
-        if n == 1 and drv.interactions_on:      # same launch sequence as kbe_step
-            _lib.check(L.kbe_sigma_frontier(P, 0, 0, sp))
-        for ci, (nf, it) in enumerate(calls):
+        for ci, (nf, it) in enumerate(calls):   # same launch sequence as kbe_step
+            if drv.interactions_on:
+                _lib.check(L.kbe_sigma_frontier(P, nf, it, sp))
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(st)
             _lib.check(L.kbe_collision_frontier(P, nf, it, sp))
             e1.record(st)
             ev.append((n, ci, nf, e0, e1))
-            if ci == 0:
-                _lib.check(L.kbe_update_sigma(P, n, 0, 0, sp))
-            else:
-                _lib.check(L.kbe_update_sigma(P, n, 1, it, sp))
+            _lib.check(L.kbe_update(P, n, 0 if ci == 0 else 1, it, sp))
         _lib.check(L.kbe_finish_step(P, n, sp))
     t_total1.record(st)
     torch.cuda.synchronize()
@@ -253,6 +287,7 @@ def run_ours(args):
     model, cfg = _make_driver(kb)
     grid = kb.build_kgrid(CFG["n_k"])
     drv = kb.PropagationDriver(grid, model, cfg)
+    hist_gb = 2 * drv.ws.g_hist.numel() * 16 / 1e9
     st = torch.cuda.current_stream()
     N = CFG["n_steps"]
 
@@ -289,10 +324,10 @@ def run_ours(args):
     iters = reps[:, 1].astype(int)
     dens = reps[:, 5] / CFG["n_k"]
     value = args.steps * N / secs
-    # kbe_step: (1 + max_iter) x (K2 collision, K3 update+Sigma) + K4 finish; step 1 adds
-    # the ground state's Sigma(0); each propagation adds kbe_init_history's 2 kernels
-    per_step_launches = (1 + cfg.max_iter) * 2 + 1
-    gpu_launches = args.steps * (N * per_step_launches + (1 if drv.interactions_on else 0) + 2)
+    # kbe_step: (1 + max_iter) x (K1 Sigma, K2 collision, K3 update) + K4 finish; each
+    # propagation adds kbe_init_history's 2 kernels
+    per_step_launches = (1 + cfg.max_iter) * (3 if drv.interactions_on else 2) + 1
+    gpu_launches = args.steps * (N * per_step_launches + 2)
 
     # e2e: public API with host inputs (model tables in, StepReports out)
     torch.cuda.synchronize()
@@ -330,8 +365,8 @@ def run_ours(args):
             "data": "synthetic (reference model defaults, deterministic; no dataset)",
             "config": {"workload": WORKLOAD, "n_k": CFG["n_k"], "n_steps": N, "dt": CFG["dt"], "U": CFG["u"],
                        "pulse": [CFG["pulse_intensity"], CFG["pulse_center"]],
-                       "parallelism": f"k-shards x{world}", "bench_step": "one whole 1000-step propagation",
-                       "l2": "inputs larger than L2 (2 GB device history per propagation)"},
+                       "parallelism": f"k-shards x{world}", "bench_step": f"one whole {N}-step propagation",
+                       "l2": f"inputs larger than L2 ({hist_gb:.2f} GB device history per propagation)"},
             "e2e": {"value": N / e2e_s, "unit": "time-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "paper_2505_19467_b200.run(grid, model, step_cfg)"},
             "gpu_launches": gpu_launches,
@@ -373,7 +408,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="BASELINE.json config (cfg2 = configs[1], the headline line)")
     args = ap.parse_args()
+    select_workload(args.workload)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -94,13 +94,6 @@ typedef struct kbe_problem {
     void* lc_part;        /* [k_local][nbb][N+1][4]: I< column, row-direction sums  */
     void* gc_part_c;      /* [k_local][nsb][N+1][4]: I> column, column-direction    */
     void* lc_part_c;      /* [k_local][nsb][N+1][4]: I< column, column-direction    */
-    /* Fresh Sigma frontier (NULL: none; one rank, U != 0 only): [k_local][8][plane_len(N)].
-     * kbe_update_sigma writes Sigma(t_n, .) of the G iterate it just produced here
-     * and moves the Sigma the collision just consumed into the history, so that
-     * the history always holds what the reference's SigmaHistory holds (Sigma of
-     * the last EVALUATED iterate) while kbe_collision_frontier(n >= 1) reads the
-     * Sigma frontier slice from this buffer. */
-    void* s_fresh;
 } kbe_problem;
 
 /* ---- layout helpers (host-callable, no device work) ---------------------- */
@@ -155,12 +148,6 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
  * h(k; t_{n-1/2}) (model.py:123-152). */
 int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
 
-/* kbe_update fused with evaluate_sigma_batched (selfenergy.py:261-325) of the
- * updated frontier: the CTA that writes G(t_n, t_b) for all k of its points b
- * evaluates the second-Born Sigma(t_n, t_b) of those pairs (+ the diagonal) in
- * the same launch.  One rank only (all k local).  With U == 0 it is kbe_update. */
-int kbe_update_sigma(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream);
-
 /* k-mean of rho for hf_mode="on" (model.py:106-120): phase 0 uses
  * rho(t_{n-1}), phase 1 uses (rho(t_{n-1}) + rho(t_n))/2.  Local k sum;
  * the caller all-reduces across ranks before dividing (kbe_hf_finalize). */
@@ -177,9 +164,8 @@ int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream);
 int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream);
 
 /* One whole PropagationDriver.step() (propagator.py:316-382) on one rank:
- * Sigma(n-1), I(n-1), predictor, max_iter x (Sigma(n), I(n), corrector), finish.
- * Sigma(n-1) and every Sigma(n) come out of kbe_update_sigma; only step 1 runs
- * the standalone kbe_sigma_frontier for the ground state's Sigma(0). */
+ * Sigma(n-1), I(n-1), predictor, max_iter x (Sigma(n), I(n), corrector), finish
+ * (kbe_sigma_frontier, kbe_collision_frontier, kbe_update, kbe_finish_step). */
 int kbe_step(const kbe_problem* p, int32_t n, void* stream);
 
 /* Steps n_first..n_last (inclusive) back to back (PropagationDriver.run,

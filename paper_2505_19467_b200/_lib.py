@@ -20,7 +20,7 @@ TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -44,7 +44,6 @@ class KbeProblem(ctypes.Structure):
         ("front_send", _p), ("front_all", _p),
         ("ctl", _p), ("reports", _p), ("phi", _p),
         ("row_part_g", _p), ("col_part_g", _p), ("lc_part", _p), ("gc_part_c", _p), ("lc_part_c", _p),
-        ("s_fresh", _p),
     ]
 
 
@@ -63,7 +62,6 @@ SIGNATURES = {
     "kbe_collision_frontier": (ctypes.c_int, [_p, _i32, _i32, _p]),
     "kbe_collision_slice": (ctypes.c_int, [_p, _i32, _p, _p, _p, _p, _p]),
     "kbe_update": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
-    "kbe_update_sigma": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_hf_mean": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_build_phi": (ctypes.c_int, [_p, _i32, _i32, _p]),
     "kbe_finish_step": (ctypes.c_int, [_p, _i32, _p]),

@@ -23,7 +23,7 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 2
+#define KBE_ABI_VERSION 3
 
 typedef double2 cplx;
 
@@ -261,31 +261,86 @@ __device__ __forceinline__ cplx sig_s2(const cplx* gp, const cplx* Xm, int nk, i
     return acc;
 }
 
-// K1 launch shape: 8*n_k threads per pair (one per (component, jm, q)); small n_k
-// packs several pairs per 128-thread CTA.
-__host__ __device__ __forceinline__ int sigma_threads(int nk) { return 8 * nk < 128 ? 128 : 8 * nk; }
-__host__ __device__ __forceinline__ int sigma_pairs_per_block(int nk) { return sigma_threads(nk) / (8 * nk); }
-static size_t sigma_smem_bytes(int nk, int pb) { return (size_t)24 * pb * nk * sizeof(cplx); }
+// ---- K1 on the step frontier: register-blocked circular correlations ----------------
+// Every stage of the factorised Sigma is a length-n_k circular correlation
+//   out[r] = sum_t C[t] A[(a0 + DT t + DR r) mod n_k],  r = 0..R-1,
+// with C walked in lock-step by all lanes of a correlation (a shared-memory
+// broadcast) and A read through a sliding window of R registers: one new A element
+// per t feeds R complex FMAs.  A operands are stored "unrolled" (duplicated past
+// n_k with the rotation the stage needs) so no index wraps, and padded by one
+// element every 8 (sg_pad) so that lanes R elements apart hit distinct banks.
+// R = 4 (2 when 4 does not divide n_k) keeps the FP64 pipe, not shared memory,
+// the limiter: per t a warp issues 4R DFMA and two loads.
+__host__ __device__ __forceinline__ int sg_pad(int j) { return j + (j >> 3); }
+__host__ __device__ __forceinline__ int sg_r(int nk) { return (nk & 3) ? 2 : 4; }
+// half-pair = (pair b, component); shared-memory layout (complex elements):
+//   DG[4][LDG]  gp_jm: DG[jm][pad(j)] = gp_jm[(j - h) mod n_k], j < 2 n_k + h
+//   DR[4][LDG]  gr_jm, same rotation
+//   PM[4][LDP]  P_jm(q) at pad(q)
+//   DX[4][LDX]  X_jm:  DX[jm][pad(j)] = X_jm[j mod n_k], j <= 2 n_k
+//   S1[4][LDP]  pref * Sigma1 of the local k (stage-2 hand-off)
+struct SgDims {
+    int nk, h, R, ldg, ldp, ldx, per;   // per = complex elements per half-pair
+    __host__ __device__ SgDims(int n_k) : nk(n_k), h(n_k >> 1), R(sg_r(n_k)) {
+        ldg = sg_pad(2 * nk + h - 1) + 1;
+        ldp = sg_pad(nk - 1) + 1;
+        ldx = sg_pad(2 * nk) + 1;
+        per = 8 * ldg + 8 * ldp + 4 * ldx;
+    }
+};
+// half-pairs per CTA: 256 threads over 8 n_k / R stage-1 tasks each
+__host__ __device__ __forceinline__ int sigma_hp_per_block(int nk) {
+    const int t = 8 * nk / sg_r(nk);
+    return t >= 256 ? 1 : 256 / t;
+}
+static size_t sigma_smem_bytes(int nk) { return (size_t)sigma_hp_per_block(nk) * SgDims(nk).per * sizeof(cplx); }
+#define SIGMA_THREADS 256
+
+template <int R, int DT, int DR>
+__device__ __forceinline__ void sg_corr(const cplx* __restrict__ A, int a0, const cplx* __restrict__ C, int c0, int nk,
+                                        cplx* acc) {
+    cplx w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r] = A[sg_pad(a0 + DR * r)];
+    for (int t0 = 0; t0 < nk; t0 += R) {
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int t = t0 + u;
+            const cplx c = C[sg_pad(c0 + t)];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int slot = (DT == DR) ? (r + u) % R : ((r - u) % R + R) % R;
+                acc[r] = cfma(w[slot], c, acc[r]);
+            }
+            // slide to t+1: the element that left the window is replaced by the new one
+            if (DT == DR) w[u] = A[sg_pad(a0 + DT * (t + 1) + DR * (R - 1))];
+            else w[R - 1 - u] = A[sg_pad(a0 + DT * (t + 1))];
+        }
+    }
+}
 
 // K1: both components of Sigma on the step-n frontier (evaluate_sigma_batched,
 // selfenergy.py:261-325).  Pair b uses G<(t_b,t_n) and G>(t_n,t_b), read from the
 // G frontier slice n for ALL k (gathered buffer on >1 rank).
 //   lesser  (primary G<(b,n), reversed G>(n,b)) -> S<(t_b,t_n) = upper planes 4..7
 //   greater (primary G>(n,b), reversed G<(b,n)) -> S>(t_n,t_b) = lower planes 0..3
-__global__ void __launch_bounds__(1024) sigma_frontier_kernel(kbe_problem P, int n, int it) {
+// One CTA = sigma_hp_per_block(n_k) half-pairs (pair, component); stage 1 computes
+// P and X (selfenergy.py:59-94 and the inner sum of 139-203), stage 2 Sigma1 and
+// Sigma2 for the local k (selfenergy.py:104-136, 139-203), Sigma = Sigma1 - Sigma2.
+template <int R>
+__global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (kbe_skip(ctl, it, P.eps)) return;
     extern __shared__ cplx sm[];
     const int nk = P.n_k;
-    const int PB = sigma_pairs_per_block(nk);
-    const int b0 = blockIdx.x * PB;
-    const int np = min(PB, n + 1 - b0);
+    const SgDims D(nk);
+    const int h = D.h;
+    const int HB = sigma_hp_per_block(nk);
+    const int hp0 = blockIdx.x * HB;
+    const int nhp = min(HB, 2 * (n + 1) - hp0);
     const int nloc = P.k_hi - P.k_lo;
-    cplx* V1 = sm;                       // [PB][4][nk]  G<(t_b,t_n)
-    cplx* V2 = V1 + PB * nk * 4;         // [PB][4][nk]  G>(t_n,t_b)
-    cplx* PX = V2 + PB * nk * 4;         // [PB][2 comp][2 (P,X)][4][nk]
-    const int tid = threadIdx.x, nth = blockDim.x;
+    const int tid = threadIdx.x;
 
     // frontier source: [k][8 planes][stride]
     const cplx* src;
@@ -299,39 +354,98 @@ __global__ void __launch_bounds__(1024) sigma_frontier_kernel(kbe_problem P, int
         pstride = plane_len(n);
         kstride = P.tri;
     }
-    // load + transform: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
-    for (int i = tid; i < np * nk * 8; i += nth) {
-        const int p = i % np, c = (i / np) & 7, k = i / (np * 8);
-        const int b = b0 + p;
-        const cplx v = __ldg(src + k * kstride + c * pstride + b);
+    // stage 0: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
+    // comp 0: gp = V1, gr = V2;  comp 1: gp = V2, gr = V1 (each half-pair loads both).
+    for (int i = tid; i < nhp * 8 * nk; i += SIGMA_THREADS) {
+        const int p = i % nhp, c = (i / nhp) & 7, k = i / (nhp * 8);
+        const int hp = hp0 + p, b = hp >> 1, comp = hp & 1;
         const int cc = c & 3;
-        cplx* dst = (c < 4 ? V1 : V2) + p * nk * 4;
-        if (b < n) dst[((cc & 1) * 2 + (cc >> 1)) * nk + k] = cneg(cconj(v));
-        else dst[cc * nk + k] = v;
+        const cplx v = __ldg(src + k * kstride + c * pstride + b);
+        const cplx x = b < n ? cneg(cconj(v)) : v;
+        const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
+        const bool is_gp = (c < 4) == (comp == 0);
+        cplx* dst = sm + (int64_t)p * D.per + (is_gp ? 0 : 4 * D.ldg) + jm * D.ldg;
+        const int j = k + h;
+        dst[sg_pad(j)] = x;
+        dst[sg_pad(j + nk)] = x;
+        if (j >= nk) dst[sg_pad(j - nk)] = x;
     }
     __syncthreads();
-    const int per = 8 * nk;
-    const int p = tid / per, r = tid % per;
-    const int comp = r / (4 * nk), jm = (r / nk) & 3, q = r % nk;
-    const bool act = p < np;
-    const cplx* gp = (comp == 0 ? V1 : V2) + p * nk * 4;
-    const cplx* gr = (comp == 0 ? V2 : V1) + p * nk * 4;
-    cplx* base = PX + (p * 2 + comp) * 8 * nk;
-    // stage 1: P and X, one (component, jm, q) per thread
-    if (act) {
-        base[jm * nk + q] = sig_pol(gp, gr, nk, jm, q);
-        base[4 * nk + jm * nk + q] = sig_x(gp, gr, nk, jm, q);
+
+    // stage 1: P_jm(q) (f < 4) and X_jm(d) (f >= 4), R consecutive outputs per task
+    const int NB = nk / R;
+    for (int task = tid; task < nhp * 8 * NB; task += SIGMA_THREADS) {
+        const int p = task / (8 * NB), f = (task / NB) & 7, blk = task % NB;
+        cplx* base = sm + (int64_t)p * D.per;
+        const cplx* DG = base;
+        const cplx* DRr = base + 4 * D.ldg;
+        cplx* PM = base + 8 * D.ldg;
+        cplx* DX = PM + 4 * D.ldp;
+        const int jm = f & 3, j = jm >> 1, m = jm & 1, o0 = blk * R;
+        cplx acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = cz();
+        if (f < 4) {   // P_jm(q) = sum_t gp_jm[t+q-h] gr_mj[t]
+            sg_corr<R, 1, 1>(DG + jm * D.ldg, o0, DRr + (m * 2 + j) * D.ldg, h, nk, acc);
+#pragma unroll
+            for (int r = 0; r < R; ++r) PM[jm * D.ldp + sg_pad(o0 + r)] = acc[r];
+        } else {       // X_jm(d) = sum_t gr_{m'j'}[d+t] gp_{j'm}[t]
+            sg_corr<R, 1, 1>(DRr + ((1 - m) * 2 + (1 - j)) * D.ldg, o0 + h, DG + ((1 - j) * 2 + m) * D.ldg, h, nk, acc);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                DX[jm * D.ldx + sg_pad(o0 + r)] = acc[r];
+                DX[jm * D.ldx + sg_pad(o0 + r + nk)] = acc[r];
+            }
+            if (o0 == 0) DX[jm * D.ldx + sg_pad(2 * nk)] = acc[0];
+        }
     }
     __syncthreads();
-    // stage 2: S1 - S2 on local k (q indexes the local k)
-    if (act && q < nloc) {
-        const int k = P.k_lo + q, b = b0 + p;
-        const double pref = (P.u_table[b] * P.u_table[n]) / ((double)nk * (double)nk);
-        const cplx s1 = cscale(sig_s1(base, gp, nk, jm, k), pref);
-        const cplx s2 = cscale(sig_s2(gp, base + 4 * nk, nk, jm, k), pref);
+
+    // stage 2: Sigma1 (which = 0) and Sigma2 (which = 1) for R consecutive local k
+    const int NBL = (nloc + R - 1) / R;
+    const double inv2 = 1.0 / ((double)nk * (double)nk);
+    cplx s2v[R];
+    int s2_task = -1;
+    for (int task = tid; task < nhp * 8 * NBL; task += SIGMA_THREADS) {
+        const int p = task / (8 * NBL), which = (task / (4 * NBL)) & 1, jm = (task / NBL) & 3, blk = task % NBL;
+        const int hp = hp0 + p, b = hp >> 1;
+        cplx* base = sm + (int64_t)p * D.per;
+        const cplx* DG = base;
+        const cplx* PM = base + 8 * D.ldg;
+        const cplx* DX = PM + 4 * D.ldp;
+        cplx* S1 = (cplx*)DX + 4 * D.ldx;
+        const int j = jm >> 1, m = jm & 1;
+        const int k0 = min(P.k_lo + blk * R, nk - R);   // global k of output r = 0
+        const double pref = (P.u_table[b] * P.u_table[n]) * inv2;
+        cplx acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = cz();
+        if (which == 0) {   // S1_jm(k) = sum_t P_{j'm'}[t] gp_jm[k-t+h]
+            sg_corr<R, -1, 1>(DG + jm * D.ldg, k0 + nk, PM + (3 - jm) * D.ldp, 0, nk, acc);
+#pragma unroll
+            for (int r = 0; r < R; ++r) S1[jm * D.ldp + sg_pad(k0 + r)] = cscale(acc[r], pref);
+        } else {            // S2_jm(k) = sum_t gp_{jm'}[t] X_jm[t-k]
+            sg_corr<R, 1, -1>(DX + jm * D.ldx, nk - k0, DG + (j * 2 + (1 - m)) * D.ldg, h, nk, acc);
+#pragma unroll
+            for (int r = 0; r < R; ++r) s2v[r] = cscale(acc[r], pref);
+            s2_task = task;
+        }
+    }
+    __syncthreads();
+    if (s2_task >= 0) {   // one stage-2 task per thread at most (8 NBL <= 256 per half-pair)
+        const int task = s2_task;
+        const int p = task / (8 * NBL), jm = (task / NBL) & 3, blk = task % NBL;
+        const int hp = hp0 + p, b = hp >> 1, comp = hp & 1;
+        const cplx* S1 = sm + (int64_t)p * D.per + 8 * D.ldg + 4 * D.ldp + 4 * D.ldx;
+        const int k0 = min(P.k_lo + blk * R, nk - R);
+        const int lo = P.k_lo + blk * R, hi = min(P.k_lo + (blk + 1) * R, P.k_hi);
         const int plane = comp == 0 ? 4 + jm : jm;
-        cplx* dst = (cplx*)P.s_hist + slice_off(n);
-        dst[(int64_t)q * P.tri + plane * plane_len(n) + b] = csub(s1, s2);
+        cplx* dst = (cplx*)P.s_hist + slice_off(n) + plane * plane_len(n) + b;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int k = k0 + r;
+            if (k >= lo && k < hi) dst[(int64_t)(k - P.k_lo) * P.tri] = csub(S1[jm * D.ldp + sg_pad(k)], s2v[r]);
+        }
     }
 }
 
@@ -483,36 +597,16 @@ struct CollSmem {
     uint64_t bar[KBE_STAGES];
 };
 
-// A streamed triangle: slices live in the packed history, except that slice alt_s
-// may be redirected to a side buffer (the fresh Sigma frontier, see s_fresh).
-struct SliceSrc {
-    const cplx* hist;
-    const cplx* alt;   // NULL: no redirection
-    int alt_s;
-    int64_t alt_pl;    // plane stride of the side buffer
-};
-// Issue the 8 plane copies of slice s, points [wb0, wb0+32) clipped to the plane.
-__device__ __forceinline__ void issue_slice(const SliceSrc& src, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
+// Issue the 8 plane copies of history slice s, points [wb0, wb0+32) clipped to the plane.
+__device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
                                             uint64_t pol) {
     const int64_t pl = plane_len(s);
     const int cnt = (int)min((int64_t)32, pl - wb0);
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_expect_tx(bar, 8u * bytes);
-    const bool redirect = src.alt && s == src.alt_s;
-    const cplx* base = (redirect ? src.alt : src.hist + slice_off(s)) + wb0;
-    const int64_t stride = redirect ? src.alt_pl : pl;
+    const cplx* base = hist + slice_off(s) + wb0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * stride, bytes, bar, pol);
-}
-// Sigma frontier source of K2 at frontier n: the side buffer s_fresh (written by the
-// fused update, kbe_update_sigma) when present, else Sigma slice n of the history.
-__device__ __forceinline__ const cplx* sigma_front(const kbe_problem& P, int kl, int n, int64_t& pl) {
-    if (P.s_fresh && n >= 1) {
-        pl = plane_len(P.n_steps);
-        return (const cplx*)P.s_fresh + (int64_t)kl * 8 * pl;
-    }
-    pl = plane_len(n);
-    return (const cplx*)P.s_hist + (int64_t)kl * P.tri + slice_off(n);
+    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar, pol);
 }
 
 // triangular index t -> (sc, bc) with 0 <= bc <= sc
@@ -568,12 +662,10 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         const int b = wb0 + lane;
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        int64_t spl;
-        const cplx* sfr = sigma_front(P, kl, n, spl);
         // frontier slice n (vector) and the streamed triangle
-        const cplx* fr = part == 0 ? G + slice_off(n) : sfr;
-        const int64_t pln = part == 0 ? plane_len(n) : spl;
-        const SliceSrc hist = part == 0 ? SliceSrc{S, sfr, n, spl} : SliceSrc{G, nullptr, -1, 0};
+        const cplx* fr = (part == 0 ? G : S) + slice_off(n);
+        const int64_t pln = plane_len(n);
+        const cplx* hist = part == 0 ? S : G;
         __syncwarp();
         if (lane == 0)
             for (int i = 0; i < KBE_STAGES && i < m; ++i) {
@@ -759,11 +851,9 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
         const int b = wb0 + lane;
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        int64_t spl;
-        const cplx* sfr = sigma_front(P, kl, n, spl);
-        const cplx* fr = part == 0 ? G + slice_off(n) : sfr;
-        const int64_t pln = part == 0 ? plane_len(n) : spl;
-        const SliceSrc hist = part == 0 ? SliceSrc{S, sfr, n, spl} : SliceSrc{G, nullptr, -1, 0};
+        const cplx* fr = (part == 0 ? G : S) + slice_off(n);
+        const int64_t pln = plane_len(n);
+        const cplx* hist = part == 0 ? S : G;
         __syncwarp();
         if (lane == 0)
             for (int i = 0; i < KBE_STAGES && i < m; ++i) {
@@ -1073,8 +1163,7 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
     mm_bdag(out, src, phi);
 }
 
-// K3: predictor / corrector / residual for the frontier points of ALL local k,
-// optionally fused with K1 (the Sigma slice of the updated frontier).
+// K3: predictor / corrector / residual for the frontier points of ALL local k.
 //
 // One CTA owns PPC consecutive frontier points b for every local k; thread =
 // (k, point, block entry), so that a warp reads whole 64-byte blocks of PPC
@@ -1082,12 +1171,7 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
 // the K2 partials of its block entry in chunk order (deterministic).  Phase B: it
 // applies Phi (G - i dt I) / (G + i dt I) Phi^dag (propagator.py:154-158,
 // 182-191).  The CTA holding b = n-1 also does the equal-time diagonal b = n
-// (propagator.py:193-212).  Phase C (SIGMA, one rank): the CTA now holds the new
-// G(t_n, t_b) of all k for its points (+ the diagonal), which is exactly what the
-// second-Born Sigma of those pairs needs, so it evaluates Sigma(n) there (K1's
-// math, selfenergy.py:59-325) instead of a separate launch.  That Sigma is the one
-// the next corrector iteration reads, and - for the last iteration - the Sigma(n)
-// that step n+1 starts from (propagator.py:331-333).
+// (propagator.py:193-212).
 // LANG = limit_mode (langreth): a template parameter so that the as-printed kernel
 // does not carry the langreth reductions' registers.
 // Points per CTA: up to 4 (and <= 512 threads), but small frontiers keep one point
@@ -1104,14 +1188,12 @@ static int upd_ppc(int nkl, int n) {
     return p;
 }
 static int upd_threads(int nkl, int ppc) { return ((ppc * 4 * nkl + 31) / 32) * 32; }
-static size_t upd_smem_bytes(int nkl, int nk, int ppc) {
+static size_t upd_smem_bytes(int nkl, int ppc) {
     return sizeof(cplx) * ((size_t)2 * ppc * nkl * 4          // sA, sB
-                           + (size_t)6 * nkl * 4              // sC, sRow, sCol, sX, sY, sZ
-                           + (size_t)2 * (ppc + 1) * 4 * nk   // V1, V2 (Sigma operands)
-                           + (size_t)(ppc + 1) * 16 * nk);    // P, X per component
+                           + (size_t)6 * nkl * 4);            // sC, sRow, sCol, sX, sY, sZ
 }
 
-template <int LANG, int SIGMA>
+template <int LANG>
 __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
@@ -1120,7 +1202,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     } else if (kbe_skip(ctl, it, P.eps)) {
         return;
     }
-    const int nkl = P.k_hi - P.k_lo, nk = P.n_k;
+    const int nkl = P.k_hi - P.k_lo;
     const int tid = threadIdx.x, T = blockDim.x;
     const int b0 = blockIdx.x * PPC;
     const int np = min(PPC, n - b0);           // own points b0 .. b0+np-1 (all < n)
@@ -1138,9 +1220,6 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     cplx* sX = sCol + nkl * 4;                   // [nkl][4]       langreth extras
     cplx* sY = sX + nkl * 4;
     cplx* sZ = sY + nkl * 4;
-    cplx* V1 = sZ + nkl * 4;                     // [PPC+1][4][nk] G<(t_b, t_n)
-    cplx* V2 = V1 + (PPC + 1) * 4 * nk;          // [PPC+1][4][nk] G>(t_n, t_b)
-    cplx* PX = V2 + (PPC + 1) * 4 * nk;          // [PPC+1][2 comp][2 (P,X)][4][nk]
     __shared__ double red[32];
     __shared__ int redf[32];
     if (phase == 0 && blockIdx.x == 0 && tid < KBE_MAX_ITER) {
@@ -1196,17 +1275,20 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         const int c0 = b / cts;
         const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
         const int na = nr + ns, ng = b < nf ? (LANG ? nr + ns : nr) : 0;
+        // UPD_BATCH independent loads per operand in flight before the in-order adds
+        // (the sum order, and so the result, does not depend on the batch size)
+        constexpr int UPD_BATCH = 4;
         cplx a = cz(), g = cz();
-        for (int i0 = 0; i0 < na || i0 < ng; i0 += 4) {
-            cplx va[4], vg[4];
+        for (int i0 = 0; i0 < na || i0 < ng; i0 += UPD_BATCH) {
+            cplx va[UPD_BATCH], vg[UPD_BATCH];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < UPD_BATCH; ++u) {
                 const int q = i0 + u;
                 va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
                 vg[u] = q < ng ? (q < nr ? gcP[q * cs] : gcC[(c0 + q - nr) * cs]) : cz();
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < UPD_BATCH; ++u) {
                 if (i0 + u < na) a = cadd(a, va[u]);
                 if (i0 + u < ng) g = cadd(g, vg[u]);
             }
@@ -1300,11 +1382,6 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             fs[c * pm + b] = row;
             fs[(4 + c) * pm + b] = col;
         }
-        if (SIGMA) {   // Sigma operands of pair b: G<(t_b,t_n) = -row^dag, G>(t_n,t_b) = -col^dag
-            const int t = (c & 1) * 2 + (c >> 1);
-            V1[(o * 4 + t) * nk + P.k_lo + kl] = cneg(cconj(row));
-            V2[(o * 4 + t) * nk + P.k_lo + kl] = cneg(cconj(col));
-        }
     }
     if (diag_cta) {
         __syncthreads();   // sRow / sCol of point n-1
@@ -1372,10 +1449,6 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 fs[e * pm + n] = nl;
                 fs[(4 + e) * pm + n] = nu;
             }
-            if (SIGMA) {   // pair n: G<(t_n,t_n), G>(t_n,t_n) as stored
-                V1[(PPC * 4 + e) * nk + P.k_lo + kl] = nl;
-                V2[(PPC * 4 + e) * nk + P.k_lo + kl] = nu;
-            }
         }
     }
     if (phase == 1) {
@@ -1400,62 +1473,6 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         }
     }
 
-    // ---- phase C: Sigma(n) of the CTA's pairs (own points + the diagonal) ----------------
-    if (SIGMA) {
-        __syncthreads();
-        const int nslot = PPC + 1;
-        auto slot_b = [&](int p) -> int { return p < PPC ? (p < np ? b0 + p : -1) : (diag_cta ? n : -1); };
-        const int64_t pmf = plane_len(P.n_steps);
-        if (phase == 0 && P.s_fresh && n >= 2) {
-            // predictor of step n: the fresh Sigma(n-1) the step started from (consumed by
-            // collision(n-1)) is the reference's Sigma slice n-1 (propagator.py:331-333).
-            // The CTAs' own points 0..n-1 cover the whole slice.  (Stage 2 rewrites
-            // s_fresh only after the barrier below.)
-            cplx* hp = (cplx*)P.s_hist + slice_off(n - 1);
-            const int64_t plq = plane_len(n - 1);
-            for (int item = tid; item < np * 8 * nkl; item += T) {
-                const int kl = item % nkl, plane = (item / nkl) & 7, b = b0 + item / (8 * nkl);
-                hp[(int64_t)kl * P.tri + plane * plq + b] = ((const cplx*)P.s_fresh)[((int64_t)kl * 8 + plane) * pmf + b];
-            }
-        }
-        // stage 1: P and X, one (pair, component, jm, q) per item
-        for (int item = tid; item < nslot * 8 * nk; item += T) {
-            const int q = item % nk, jm = (item / nk) & 3, comp = (item / (4 * nk)) & 1, p = item / (8 * nk);
-            if (slot_b(p) < 0) continue;
-            const cplx* gp = (comp == 0 ? V1 : V2) + p * 4 * nk;
-            const cplx* gr = (comp == 0 ? V2 : V1) + p * 4 * nk;
-            cplx* base = PX + (p * 2 + comp) * 8 * nk;
-            base[jm * nk + q] = sig_pol(gp, gr, nk, jm, q);
-            base[4 * nk + jm * nk + q] = sig_x(gp, gr, nk, jm, q);
-        }
-        __syncthreads();
-        // stage 2: Sigma1 - Sigma2 on the local k, written to Sigma slice n
-        cplx* dst0 = (cplx*)P.s_hist + slice_off(n);
-
-        for (int item = tid; item < nslot * 8 * nkl; item += T) {
-            const int kl = item % nkl, jm = (item / nkl) & 3, comp = (item / (4 * nkl)) & 1, p = item / (8 * nkl);
-            const int b = slot_b(p);
-            if (b < 0) continue;
-            const cplx* gp = (comp == 0 ? V1 : V2) + p * 4 * nk;
-            const cplx* base = PX + (p * 2 + comp) * 8 * nk;
-            const int k = P.k_lo + kl;
-            const double pref = (P.u_table[b] * P.u_table[n]) / ((double)nk * (double)nk);
-            const cplx s1 = cscale(sig_s1(base, gp, nk, jm, k), pref);
-            const cplx s2 = cscale(sig_s2(gp, base + 4 * nk, nk, jm, k), pref);
-            const int plane = comp == 0 ? 4 + jm : jm;
-            const cplx v = csub(s1, s2);
-            if (P.s_fresh) {
-                // the Sigma the collision just consumed becomes the history's slice
-                // (reference state: Sigma(n) of the last evaluated iterate); the new
-                // one waits in s_fresh for the next collision
-                cplx* f = (cplx*)P.s_fresh + ((int64_t)kl * 8 + plane) * pmf + b;
-                if (phase == 1) dst0[(int64_t)kl * P.tri + plane * plc + b] = *f;
-                *f = v;
-            } else {
-                dst0[(int64_t)kl * P.tri + plane * plc + b] = v;
-            }
-        }
-    }
 }
 
 // Phi(t_{n-1/2}, k) for steps n in [n0, n1], local k (hf term from ctl->hf_sum when hf_mode="on")
@@ -1657,7 +1674,9 @@ static int ensure_attrs() {
     if (g_attr_done) return KBE_OK;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(sigma_frontier_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
@@ -1671,9 +1690,8 @@ static int ensure_attrs() {
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
     {
-        void (*upd[4])(kbe_problem, int, int, int, int) = {update_kernel<0, 0>, update_kernel<0, 1>, update_kernel<1, 0>,
-                                                      update_kernel<1, 1>};
-        for (int i = 0; i < 4; ++i) {
+        void (*upd[2])(kbe_problem, int, int, int, int) = {update_kernel<0>, update_kernel<1>};
+        for (int i = 0; i < 2; ++i) {
             e = cudaFuncSetAttribute(upd[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(update)", e); return KBE_ERR_CUDA; }
         }
@@ -1695,26 +1713,21 @@ static int check_problem(const kbe_problem* p) {
         return KBE_ERR_ARG;
     }
     if (p->n_k > 128) {
-        snprintf(g_err, sizeof(g_err), "n_k > 128 is not supported by the fused Sigma kernel (one CTA per pair)");
+        snprintf(g_err, sizeof(g_err), "n_k > 128 is not supported by the Sigma kernel (one stage-2 task per thread)");
         return KBE_ERR_UNSUPPORTED;
     }
     if (!p->phi) { set_err("kbe_problem.phi", cudaSuccess); return KBE_ERR_ARG; }
     return KBE_OK;
 }
 
-static int launch_update(const kbe_problem* p, int n, int phase, int it, int sigma, void* stream) {
+static int launch_update(const kbe_problem* p, int n, int phase, int it, void* stream) {
     int rc = ensure_attrs();
     if (rc) return rc;
     const int nkl = p->k_hi - p->k_lo, ppc = upd_ppc(nkl, n);
     const dim3 grid((n + ppc - 1) / ppc), block(upd_threads(nkl, ppc));
-    const size_t smem = upd_smem_bytes(nkl, p->n_k, ppc);
-    if (p->limit_mode) {
-        if (sigma) KBE_LAUNCH("update_kernel", update_kernel<1, 1>, grid, block, smem, stream, *p, n, phase, it, ppc);
-        else KBE_LAUNCH("update_kernel", update_kernel<1, 0>, grid, block, smem, stream, *p, n, phase, it, ppc);
-    } else {
-        if (sigma) KBE_LAUNCH("update_kernel", update_kernel<0, 1>, grid, block, smem, stream, *p, n, phase, it, ppc);
-        else KBE_LAUNCH("update_kernel", update_kernel<0, 0>, grid, block, smem, stream, *p, n, phase, it, ppc);
-    }
+    const size_t smem = upd_smem_bytes(nkl, ppc);
+    if (p->limit_mode) KBE_LAUNCH("update_kernel", update_kernel<1>, grid, block, smem, stream, *p, n, phase, it, ppc);
+    else KBE_LAUNCH("update_kernel", update_kernel<0>, grid, block, smem, stream, *p, n, phase, it, ppc);
     return KBE_OK;
 }
 
@@ -1753,10 +1766,14 @@ int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream
         return KBE_ERR_ARG;
     }
     if ((rc = ensure_attrs())) return rc;
-    const int pb = sigma_pairs_per_block(p->n_k);
-    const int grid = (n + 1 + pb - 1) / pb;
-    KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel, dim3(grid), dim3(sigma_threads(p->n_k)),
-               sigma_smem_bytes(p->n_k, pb), stream, *p, (int)n, (int)it);
+    const int hb = sigma_hp_per_block(p->n_k);
+    const dim3 grid((2 * (n + 1) + hb - 1) / hb);
+    if (sg_r(p->n_k) == 4)
+        KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS),
+                   sigma_smem_bytes(p->n_k), stream, *p, (int)n, (int)it);
+    else
+        KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS),
+                   sigma_smem_bytes(p->n_k), stream, *p, (int)n, (int)it);
     return KBE_OK;
 }
 
@@ -1816,18 +1833,7 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    return launch_update(p, n, phase, it, 0, stream);
-}
-
-int kbe_update_sigma(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
-    int rc = check_problem(p);
-    if (rc) return rc;
-    if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update_sigma: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    if (p->k_lo != 0 || p->k_hi != p->n_k || p->front_all) {
-        snprintf(g_err, sizeof(g_err), "kbe_update_sigma: the fused Sigma needs all k on one rank");
-        return KBE_ERR_ARG;
-    }
-    return launch_update(p, n, phase, it, p->interacting ? 1 : 0, stream);
+    return launch_update(p, n, phase, it, stream);
 }
 
 int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
@@ -1860,17 +1866,17 @@ int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
         return KBE_ERR_ARG;
     }
     if (n < 1 || n > p->n_steps) { set_err("kbe_step: n", cudaSuccess); return KBE_ERR_ARG; }
-    // Sigma(n-1) was produced by the last update of step n-1 (fused, see update_kernel);
-    // only the ground state's Sigma(0) needs the standalone K1.
-    const int nold = n - 1;
-    if (nold == 0 && p->interacting && (rc = kbe_sigma_frontier(p, 0, 0, stream))) return rc;
-    if ((rc = kbe_collision_frontier(p, nold, 0, stream))) return rc;
+    // Algorithm 1 (propagator.py:328-382): Sigma(n-1), I(n-1), predictor, then
+    // max_iter x [Sigma(n), I(n), corrector]; converged iterations are no-ops.
+    if (p->interacting && (rc = kbe_sigma_frontier(p, n - 1, 0, stream))) return rc;
+    if ((rc = kbe_collision_frontier(p, n - 1, 0, stream))) return rc;
     if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
-    if ((rc = kbe_update_sigma(p, n, 0, 0, stream))) return rc;
+    if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
     for (int it = 0; it < p->max_iter; ++it) {
+        if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
         if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
         if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
-        if ((rc = kbe_update_sigma(p, n, 1, it, stream))) return rc;
+        if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
     }
     return kbe_finish_step(p, n, stream);
 }

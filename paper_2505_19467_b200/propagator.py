@@ -149,7 +149,7 @@ class _Workspace:
 
     def __init__(self, *, n_k, k_lo, k_hi, n_steps, dt, eps, max_iter, quad, limit_mode, hf,
                  interacting, dipole, eps_v, eps_c, u_table, u_mid, amp, g_hist, s_hist, device,
-                 multi_rank=False, fused_sigma=False):
+                 multi_rank=False):
         N1 = n_steps + 1
         kl = k_hi - k_lo
         self.nbb = -(-N1 // _lib.TILE_B)
@@ -173,10 +173,7 @@ class _Workspace:
         self.u_table = as_device_f64(u_table, device)
         self.u_mid = as_device_f64(u_mid, device)
         self.amp = as_device_f64(amp, device)
-        self.front_send = self.front_all = self.s_fresh = None
-        if fused_sigma and interacting and not multi_rank:
-            # fresh Sigma frontier of the fused update (include/kbe200.h, s_fresh)
-            self.s_fresh = torch.zeros((kl, 8, _lib.plane_len(n_steps)), **c128)
+        self.front_send = self.front_all = None
         if multi_rank:
             pm = _lib.plane_len(n_steps)
             self.front_send = torch.zeros((kl, 8, pm), **c128)
@@ -200,7 +197,6 @@ class _Workspace:
         p.phi = self.phi.data_ptr()
         if self.lang is not None:
             (p.row_part_g, p.col_part_g, p.lc_part, p.gc_part_c, p.lc_part_c) = [t.data_ptr() for t in self.lang]
-        p.s_fresh = self.s_fresh.data_ptr() if self.s_fresh is not None else None
         self.problem = p
 
     def problem_ptr(self) -> int:
@@ -275,7 +271,7 @@ class PropagationDriver:
             eps=step_cfg.eps, max_iter=step_cfg.max_iter, quad=quad, limit_mode=limit,
             hf=model.hf_mode == "on", interacting=self.interactions_on, dipole=complex(model.dipole),
             eps_v=eps_v, eps_c=eps_c, u_table=self.u_table, u_mid=u_mid, amp=amp,
-            g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1, fused_sigma=True)
+            g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1)
         _lib.check(_lib.lib().kbe_init_history(self.ws.problem_ptr(), stream_ptr()), "kbe_init_history")
         self.state = TwoTimeGF(nkl, self.k_lo, capacity, step_cfg.dt, g_hist, frontier=0)
         self.sigma = SigmaHistory(s_hist, capacity)
