@@ -309,7 +309,7 @@ def run_ours(args):
             _reset(kb, drv)
             n1 = N
             if world == 1:
-                _lib.check(_lib.lib().kbe_run(drv.ws.problem_ptr(), 1, n1, 0, int(st.cuda_stream)))
+                _lib.check(_lib.lib().kbe_run(drv.ws.problem_ptr(), 1, n1, drv.use_graph, int(st.cuda_stream)))
             else:
                 for n in range(1, n1 + 1):
                     drv._launch_step(n)
@@ -324,10 +324,16 @@ def run_ours(args):
     iters = reps[:, 1].astype(int)
     dens = reps[:, 5] / CFG["n_k"]
     value = args.steps * N / secs
-    # kbe_step: (1 + max_iter) x (K1 Sigma, K2 collision, K3 update) + K4 finish; each
-    # propagation adds kbe_init_history's 2 kernels
-    per_step_launches = (1 + cfg.max_iter) * (3 if drv.interactions_on else 2) + 1
-    gpu_launches = args.steps * (N * per_step_launches + 2)
+    # per evaluation K1 Sigma (interacting), K2 collision, K3 update; + K4 finish per step;
+    # each propagation adds kbe_init_history's 2 kernels.  Stream path: all max_iter
+    # corrector iterations launch (converged ones as no-ops); graph path: only the
+    # iterations that ran (the rest sit behind conditional nodes that stay off).
+    per_eval = 3 if drv.interactions_on else 2
+    if world == 1 and drv.use_graph:
+        per_prop = int(np.sum((1 + iters) * per_eval + 1)) + 2
+    else:
+        per_prop = N * ((1 + cfg.max_iter) * per_eval + 1) + 2
+    gpu_launches = args.steps * per_prop
 
     # e2e: public API with host inputs (model tables in, StepReports out)
     torch.cuda.synchronize()
@@ -370,6 +376,7 @@ def run_ours(args):
             "e2e": {"value": N / e2e_s, "unit": "time-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "paper_2505_19467_b200.run(grid, model, step_cfg)"},
             "gpu_launches": gpu_launches,
+            "launch_mode": "cuda-graph (conditional corrector)" if (world == 1 and drv.use_graph) else "stream",
             "iterations_hist": {int(k): int(v) for k, v in zip(*np.unique(iters, return_counts=True))},
             "final_density": float(dens[-1]),
             "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),

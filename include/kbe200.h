@@ -169,9 +169,16 @@ int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream);
 int kbe_step(const kbe_problem* p, int32_t n, void* stream);
 
 /* Steps n_first..n_last (inclusive) back to back (PropagationDriver.run,
- * propagator.py:384-392).  use_graph != 0 replays one captured CUDA graph per
- * step shape. */
+ * propagator.py:384-392).  use_graph = 0: kbe_step per step (converged corrector
+ * iterations launch as no-ops).  use_graph != 0 (one rank only): one CUDA graph per
+ * problem, replayed per step with its kernel nodes' arguments rewritten; corrector
+ * iterations 1..max_iter-1 sit behind IF conditional nodes that the previous
+ * iteration's update kernel enables only while the residual is > eps, so nothing
+ * is launched after convergence.  Results are bitwise identical either way. */
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream);
+
+/* Drop the step graph cached for this problem's control block (driver teardown). */
+int kbe_release(const kbe_problem* p);
 
 /* ---- layout conversion (TwoTimeGF / SigmaHistory accessors) -------------- */
 /* Rebuild the reference layout (k_local,2,2,N+1,N+1) of one function from the

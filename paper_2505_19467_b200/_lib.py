@@ -20,7 +20,7 @@ TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -67,6 +67,7 @@ SIGNATURES = {
     "kbe_finish_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_run": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
+    "kbe_release": (ctypes.c_int, [_p]),
     "kbe_unpack": (ctypes.c_int, [_p, _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "kbe_pack": (ctypes.c_int, [_p, _p, _i32, _i32, _i32, _i64, _p, _p]),
 }

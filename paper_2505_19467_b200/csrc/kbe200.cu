@@ -23,7 +23,7 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 3
+#define KBE_ABI_VERSION 4
 
 typedef double2 cplx;
 
@@ -36,6 +36,8 @@ struct kbe_ctl {
     cplx hf_sum[4];                        // k-sum of rho for hf_mode="on"
     unsigned task_next;                    // collision work queue head (reset by the last CTA)
     unsigned task_done;
+    unsigned upd_done;                     // update CTAs finished (graph mode; reset by the last CTA)
+    unsigned pad2;
 };
 
 static char g_err[512] = "";
@@ -1194,13 +1196,14 @@ static size_t upd_smem_bytes(int nkl, int ppc) {
 }
 
 template <int LANG>
-__global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC) {
+__global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC,
+                                                     cudaGraphConditionalHandle next_iter) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
         if (ctl->poisoned) return;
     } else if (kbe_skip(ctl, it, P.eps)) {
-        return;
+        return;   // graph mode: next_iter keeps its default 0, so the step ends
     }
     const int nkl = P.k_hi - P.k_lo;
     const int tid = threadIdx.x, T = blockDim.x;
@@ -1470,6 +1473,18 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
             atomicMax(&ctl->res[it], bits);
             if (nfl) atomicOr(&ctl->nonfinite[it], 1);
+            if (next_iter) {
+                // graph mode (kbe_run): the last CTA to finish decides whether the next
+                // corrector iteration's conditional body runs (propagator.py:360-368:
+                // continue while residual > eps, NaN included, up to max_iter)
+                __threadfence();
+                if (atomicAdd(&ctl->upd_done, 1u) == gridDim.x - 1) {
+                    ctl->upd_done = 0;
+                    __threadfence();
+                    const double rall = __longlong_as_double((long long)atomicOr(&ctl->res[it], 0ull));
+                    if (!(rall <= P.eps)) cudaGraphSetConditional(next_iter, 1u);
+                }
+            }
         }
     }
 
@@ -1640,30 +1655,70 @@ __global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int 
 }
 
 // =================================================================== host side
-// Launch with programmatic stream serialization (see pdl_enter); KBE_NO_PDL=1
-// falls back to plain stream order (for A/B timing).
-static int g_pdl = -1;
+// Every step-kernel launch is first described as a KSpec (function, grid, block,
+// shared memory, argument block).  The same spec is either launched on a stream
+// with programmatic stream serialization (see pdl_enter; KBE_NO_PDL=1 falls back
+// to plain stream order for A/B timing) or written into a kernel node of the
+// step graph (kbe_run).
+struct KSpec {
+    const void* func = nullptr;
+    dim3 grid, block;
+    size_t smem = 0;
+    alignas(16) unsigned char buf[sizeof(kbe_problem) + 64];
+    void* args[8];
+};
+template <typename... A, size_t... I>
+static void spec_pack(KSpec& s, std::index_sequence<I...>, A... a) {
+    size_t off = 0;
+    auto put = [&](auto v, size_t i) {
+        using T = decltype(v);
+        off = (off + alignof(T) - 1) / alignof(T) * alignof(T);
+        memcpy(s.buf + off, &v, sizeof(T));
+        s.args[i] = s.buf + off;
+        off += sizeof(T);
+    };
+    (put(a, I), ...);
+}
 template <typename... KArgs, typename... Args>
-static cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, void* stream, Args&&... args) {
+static void make_spec(KSpec& s, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
+    s.func = (const void*)kernel;
+    s.grid = grid;
+    s.block = block;
+    s.smem = smem;
+    spec_pack<KArgs...>(s, std::index_sequence_for<KArgs...>{}, static_cast<KArgs>(args)...);
+}
+static int g_pdl = -1;
+static cudaError_t launch_spec(const KSpec& s, void* stream) {
     if (g_pdl < 0) {
         const char* e = getenv("KBE_NO_PDL");
         g_pdl = (e && e[0] == '1') ? 0 : 1;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
+    cfg.gridDim = s.grid;
+    cfg.blockDim = s.block;
+    cfg.dynamicSmemBytes = s.smem;
     cfg.stream = (cudaStream_t)stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = g_pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+    return cudaLaunchKernelExC(&cfg, s.func, (void**)s.args);
 }
-#define KBE_LAUNCH(name, ...)                                              \
+static cudaKernelNodeParams node_params(const KSpec& s) {
+    cudaKernelNodeParams kp = {};
+    kp.func = (void*)s.func;
+    kp.gridDim = s.grid;
+    kp.blockDim = s.block;
+    kp.sharedMemBytes = (unsigned)s.smem;
+    kp.kernelParams = (void**)s.args;
+    kp.extra = nullptr;
+    return kp;
+}
+#define KBE_LAUNCH_SPEC(name, spec)                                        \
     do {                                                                   \
-        cudaError_t e_ = launch(__VA_ARGS__);                              \
+        cudaError_t e_ = launch_spec(spec, stream);                        \
         if (e_ != cudaSuccess) { set_err(name, e_); return KBE_ERR_CUDA; } \
     } while (0)
 static bool g_attr_done = false;
@@ -1690,7 +1745,7 @@ static int ensure_attrs() {
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
     {
-        void (*upd[2])(kbe_problem, int, int, int, int) = {update_kernel<0>, update_kernel<1>};
+        void (*upd[2])(kbe_problem, int, int, int, int, cudaGraphConditionalHandle) = {update_kernel<0>, update_kernel<1>};
         for (int i = 0; i < 2; ++i) {
             e = cudaFuncSetAttribute(upd[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(update)", e); return KBE_ERR_CUDA; }
@@ -1720,14 +1775,214 @@ static int check_problem(const kbe_problem* p) {
     return KBE_OK;
 }
 
-static int launch_update(const kbe_problem* p, int n, int phase, int it, void* stream) {
-    int rc = ensure_attrs();
-    if (rc) return rc;
+// ---- launch specs of the step kernels (shared by the stream and graph paths)
+static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
+    const int hb = sigma_hp_per_block(p->n_k);
+    const dim3 grid((2 * (n + 1) + hb - 1) / hb);
+    if (sg_r(p->n_k) == 4)
+        make_spec(s, sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS), sigma_smem_bytes(p->n_k), *p, n, it);
+    else
+        make_spec(s, sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS), sigma_smem_bytes(p->n_k), *p, n, it);
+}
+static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
+    const int nkl = p->k_hi - p->k_lo;
+    if (p->limit_mode) {
+        const int T0 = n / TS + 1;
+        const int64_t tl = 2 * (int64_t)(T0 * (T0 + 1) / 2) * nkl;
+        const int64_t cl = (int64_t)g_num_sms * g_lang_occ;
+        make_spec(s, collision_langreth_kernel, dim3((int)(tl < cl ? tl : cl)), dim3(32), sizeof(CollSmem), *p, n, it);
+        return;
+    }
+    const int64_t total = (int64_t)coll_tiles(n, nkl) * (TS / coll_ts(n, nkl, 0));
+    const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
+    make_spec(s, collision_kernel, dim3((int)(total < cap ? total : cap)), dim3(32), sizeof(CollSmem), *p, n, it);
+}
+static void spec_update(KSpec& s, const kbe_problem* p, int n, int phase, int it, cudaGraphConditionalHandle next) {
     const int nkl = p->k_hi - p->k_lo, ppc = upd_ppc(nkl, n);
     const dim3 grid((n + ppc - 1) / ppc), block(upd_threads(nkl, ppc));
     const size_t smem = upd_smem_bytes(nkl, ppc);
-    if (p->limit_mode) KBE_LAUNCH("update_kernel", update_kernel<1>, grid, block, smem, stream, *p, n, phase, it, ppc);
-    else KBE_LAUNCH("update_kernel", update_kernel<0>, grid, block, smem, stream, *p, n, phase, it, ppc);
+    if (p->limit_mode) make_spec(s, update_kernel<1>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else make_spec(s, update_kernel<0>, grid, block, smem, *p, n, phase, it, ppc, next);
+}
+static void spec_hf(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
+    make_spec(s, hf_mean_kernel, dim3(1), dim3(128), 0, *p, n, phase, it);
+}
+static void spec_finish(KSpec& s, const kbe_problem* p, int n) {
+    make_spec(s, finish_kernel, dim3(1), dim3(256), 0, *p, n);
+}
+
+// ---- step graph (kbe_run, one rank) ---------------------------------------------------
+// One executable graph per driver, replayed once per step with the kernel nodes'
+// n-dependent arguments and grids rewritten (cudaGraphExecKernelNodeSetParams):
+//
+//   Sigma(n-1) -> I(n-1) [-> hf] -> predict -> Sigma(n) -> I(n) [-> hf] -> correct(0)
+//   -> IF c1 { Sigma(n) -> I(n) [-> hf] -> correct(1) } -> ... -> IF c_{m-1} {...} -> finish
+//
+// correct(it)'s last CTA sets c_{it+1} = (residual > eps), so the corrector
+// iterations after convergence are never launched (the stream path launches
+// them as no-ops).  The handles default to 0 at every launch, so a step can
+// never run more than max_iter iterations.  Kernel -> kernel edges inside one
+// (sub)graph are programmatic (the PDL of the stream path); KBE_GRAPH_PDL=0
+// makes them full dependencies.
+enum { GR_SIGMA, GR_COLL, GR_HF, GR_UPD, GR_FIN };
+struct GNode {
+    cudaGraphNode_t node;
+    int role, phase, it;           // it = -1: the n-1 evaluation
+    cudaGraphConditionalHandle next;
+};
+struct StepGraph {
+    kbe_problem key;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    GNode nodes[4 * (KBE_MAX_ITER + 1) + 2];
+    int count = 0;
+};
+static StepGraph* g_graphs[8];
+static int g_graph_pdl = -1;
+
+static void fill_spec(KSpec& s, const kbe_problem* p, const GNode& g, int n) {
+    const int nn = g.it < 0 ? n - 1 : n, it = g.it < 0 ? 0 : g.it;
+    switch (g.role) {
+        case GR_SIGMA: spec_sigma(s, p, nn, it); break;
+        case GR_COLL: spec_collision(s, p, nn, it); break;
+        case GR_HF: spec_hf(s, p, n, g.phase, it); break;
+        case GR_UPD: spec_update(s, p, n, g.phase, it, g.next); break;
+        default: spec_finish(s, p, n); break;
+    }
+}
+
+// append a kernel node to `graph` after `prev` (nullptr: root); programmatic edge
+// when both are kernel nodes of the same graph
+static cudaError_t add_kernel(StepGraph* sg, cudaGraph_t graph, cudaGraphNode_t* prev, bool prev_is_kernel,
+                              const kbe_problem* p, GNode g, int n) {
+    KSpec s;
+    fill_spec(s, p, g, n);
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeKernel;
+    np.kernel.func = (void*)s.func;
+    np.kernel.gridDim = s.grid;
+    np.kernel.blockDim = s.block;
+    np.kernel.sharedMemBytes = (unsigned)s.smem;
+    np.kernel.kernelParams = (void**)s.args;
+    cudaGraphEdgeData ed = {};
+    if (prev_is_kernel && g_graph_pdl) {
+        ed.from_port = cudaGraphKernelNodePortProgrammatic;
+        ed.type = cudaGraphDependencyTypeProgrammatic;
+    }
+    cudaError_t e = cudaGraphAddNode_v2(&g.node, graph, *prev ? prev : nullptr, *prev ? &ed : nullptr,
+                                        *prev ? 1 : 0, &np);
+    if (e != cudaSuccess) return e;
+    sg->nodes[sg->count++] = g;
+    *prev = g.node;
+    return cudaSuccess;
+}
+
+static void destroy_graph(StepGraph* sg) {
+    if (!sg) return;
+    if (sg->exec) cudaGraphExecDestroy(sg->exec);
+    if (sg->graph) cudaGraphDestroy(sg->graph);
+    delete sg;
+}
+
+static int build_graph(const kbe_problem* p, int n, StepGraph** out) {
+    if (g_graph_pdl < 0) {
+        const char* e = getenv("KBE_GRAPH_PDL");
+        g_graph_pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    StepGraph* sg = new StepGraph();
+    sg->key = *p;
+    cudaError_t e = cudaGraphCreate(&sg->graph, 0);
+#define GCHK(what)                                                              \
+    if (e != cudaSuccess) { set_err(what, e); destroy_graph(sg); return KBE_ERR_CUDA; }
+    GCHK("cudaGraphCreate");
+    cudaGraphNode_t prev = nullptr;
+    bool pk = false;   // prev is a kernel node of the same graph
+    auto add = [&](cudaGraph_t gr, cudaGraphNode_t* pv, bool* pkk, int role, int phase, int it,
+                   cudaGraphConditionalHandle next) {
+        GNode g = {nullptr, role, phase, it, next};
+        cudaError_t r = add_kernel(sg, gr, pv, *pkk, p, g, n);
+        *pkk = true;
+        return r;
+    };
+    // predictor part: Sigma(n-1), I(n-1), predict
+    if (p->interacting && (e = add(sg->graph, &prev, &pk, GR_SIGMA, 0, -1, 0)) != cudaSuccess) GCHK("graph: sigma");
+    if ((e = add(sg->graph, &prev, &pk, GR_COLL, 0, -1, 0)) != cudaSuccess) GCHK("graph: collision");
+    if (p->hf && (e = add(sg->graph, &prev, &pk, GR_HF, 0, 0, 0)) != cudaSuccess) GCHK("graph: hf");
+    if ((e = add(sg->graph, &prev, &pk, GR_UPD, 0, 0, 0)) != cudaSuccess) GCHK("graph: predict");
+    // corrector iterations: 0 unconditionally, 1..max_iter-1 behind IF nodes
+    cudaGraphConditionalHandle h[KBE_MAX_ITER] = {};
+    for (int it = 1; it < p->max_iter; ++it) {
+        e = cudaGraphConditionalHandleCreate(&h[it], sg->graph, 0, cudaGraphCondAssignDefault);
+        GCHK("cudaGraphConditionalHandleCreate");
+    }
+    for (int it = 0; it < p->max_iter; ++it) {
+        cudaGraph_t body = sg->graph;
+        cudaGraphNode_t bprev = prev;
+        bool bpk = pk;
+        if (it > 0) {
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h[it];
+            cp.conditional.type = cudaGraphCondTypeIf;
+            cp.conditional.size = 1;
+            cudaGraphNode_t cnode;
+            e = cudaGraphAddNode(&cnode, sg->graph, &prev, 1, &cp);
+            GCHK("cudaGraphAddNode(conditional)");
+            body = cp.conditional.phGraph_out[0];
+            prev = cnode;
+            pk = false;
+            bprev = nullptr;
+            bpk = false;
+        }
+        const cudaGraphConditionalHandle next = it + 1 < p->max_iter ? h[it + 1] : 0;
+        if (p->interacting && (e = add(body, &bprev, &bpk, GR_SIGMA, 1, it, 0)) != cudaSuccess) GCHK("graph: sigma");
+        if ((e = add(body, &bprev, &bpk, GR_COLL, 1, it, 0)) != cudaSuccess) GCHK("graph: collision");
+        if (p->hf && (e = add(body, &bprev, &bpk, GR_HF, 1, it, 0)) != cudaSuccess) GCHK("graph: hf");
+        if ((e = add(body, &bprev, &bpk, GR_UPD, 1, it, next)) != cudaSuccess) GCHK("graph: correct");
+        if (it == 0) { prev = bprev; pk = bpk; }
+    }
+    if ((e = add(sg->graph, &prev, &pk, GR_FIN, 0, 0, 0)) != cudaSuccess) GCHK("graph: finish");
+    e = cudaGraphInstantiate(&sg->exec, sg->graph, 0);
+    GCHK("cudaGraphInstantiate");
+#undef GCHK
+    *out = sg;
+    return KBE_OK;
+}
+
+static bool same_problem(const kbe_problem* a, const kbe_problem* b) { return memcmp(a, b, sizeof(kbe_problem)) == 0; }
+
+static int get_graph(const kbe_problem* p, int n, StepGraph** out) {
+    for (auto& g : g_graphs)
+        if (g && same_problem(&g->key, p)) { *out = g; return KBE_OK; }
+    // reuse the slot of the same control block (a rebuilt problem), else a free one,
+    // else evict slot 0
+    int slot = -1;
+    for (int i = 0; i < 8 && slot < 0; ++i)
+        if (g_graphs[i] && g_graphs[i]->key.ctl == p->ctl) slot = i;
+    for (int i = 0; i < 8 && slot < 0; ++i)
+        if (!g_graphs[i]) slot = i;
+    if (slot < 0) slot = 0;
+    if (g_graphs[slot]) {
+        cudaDeviceSynchronize();
+        destroy_graph(g_graphs[slot]);
+        g_graphs[slot] = nullptr;
+    }
+    int rc = build_graph(p, n, &g_graphs[slot]);
+    if (rc) return rc;
+    *out = g_graphs[slot];
+    return KBE_OK;
+}
+
+static int graph_step(StepGraph* sg, const kbe_problem* p, int n, void* stream) {
+    for (int i = 0; i < sg->count; ++i) {
+        KSpec s;
+        fill_spec(s, p, sg->nodes[i], n);
+        cudaKernelNodeParams kp = node_params(s);
+        cudaError_t e = cudaGraphExecKernelNodeSetParams(sg->exec, sg->nodes[i].node, &kp);
+        if (e != cudaSuccess) { set_err("cudaGraphExecKernelNodeSetParams", e); return KBE_ERR_CUDA; }
+    }
+    cudaError_t e = cudaGraphLaunch(sg->exec, (cudaStream_t)stream);
+    if (e != cudaSuccess) { set_err("cudaGraphLaunch", e); return KBE_ERR_CUDA; }
     return KBE_OK;
 }
 
@@ -1744,16 +1999,20 @@ const char* kbe_last_error(void) { return g_err; }
 int kbe_init_history(const kbe_problem* p, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
+    if ((rc = ensure_attrs())) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t bytes = (size_t)(p->k_hi - p->k_lo) * p->tri * sizeof(cplx);
     cudaError_t e = cudaMemsetAsync(p->g_hist, 0, bytes, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->s_hist, 0, bytes, st);
     if (e != cudaSuccess) { set_err("cudaMemsetAsync(history)", e); return KBE_ERR_CUDA; }
     const int nloc = p->k_hi - p->k_lo;
-    KBE_LAUNCH("init_slice0_kernel", init_slice0_kernel, dim3((nloc + 127) / 128), dim3(128), 0, st, *p);
+    KSpec s;
+    make_spec(s, init_slice0_kernel, dim3((nloc + 127) / 128), dim3(128), 0, *p);
+    KBE_LAUNCH_SPEC("init_slice0_kernel", s);
     const int64_t cnt = (int64_t)p->n_steps * nloc;
-    KBE_LAUNCH("phi_table_kernel", phi_table_kernel, dim3((int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096)),
-               dim3(256), 0, st, *p, 1, p->n_steps, 0, 0);
+    make_spec(s, phi_table_kernel, dim3((int)((cnt + 255) / 256 < 4096 ? (cnt + 255) / 256 : 4096)), dim3(256), 0, *p,
+              1, p->n_steps, 0, 0);
+    KBE_LAUNCH_SPEC("phi_table_kernel", s);
     return KBE_OK;
 }
 
@@ -1766,14 +2025,9 @@ int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream
         return KBE_ERR_ARG;
     }
     if ((rc = ensure_attrs())) return rc;
-    const int hb = sigma_hp_per_block(p->n_k);
-    const dim3 grid((2 * (n + 1) + hb - 1) / hb);
-    if (sg_r(p->n_k) == 4)
-        KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS),
-                   sigma_smem_bytes(p->n_k), stream, *p, (int)n, (int)it);
-    else
-        KBE_LAUNCH("sigma_frontier_kernel", sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS),
-                   sigma_smem_bytes(p->n_k), stream, *p, (int)n, (int)it);
+    KSpec s;
+    spec_sigma(s, p, n, it);
+    KBE_LAUNCH_SPEC("sigma_frontier_kernel", s);
     return KBE_OK;
 }
 
@@ -1801,21 +2055,9 @@ int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* st
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
-    const int nkl = p->k_hi - p->k_lo;
-    const int64_t total = (int64_t)coll_tiles(n, nkl) * (TS / coll_ts(n, nkl, 0));
-    const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
-    const int grid = (int)(total < cap ? total : cap);
-    if (p->limit_mode)
-    {
-        const int T0 = n / TS + 1;
-        const int64_t tl = 2 * (int64_t)(T0 * (T0 + 1) / 2) * (p->k_hi - p->k_lo);
-        const int64_t cl = (int64_t)g_num_sms * g_lang_occ;
-        KBE_LAUNCH("collision_langreth_kernel", collision_langreth_kernel, dim3((int)(tl < cl ? tl : cl)), dim3(32),
-                   sizeof(CollSmem), stream, *p, (int)n, (int)it);
-    } else {
-        KBE_LAUNCH("collision_kernel", collision_kernel, dim3(grid), dim3(32), sizeof(CollSmem), stream, *p, (int)n,
-                   (int)it);
-    }
+    KSpec s;
+    spec_collision(s, p, n, it);
+    KBE_LAUNCH_SPEC(p->limit_mode ? "collision_langreth_kernel" : "collision_kernel", s);
     return KBE_OK;
 }
 
@@ -1823,9 +2065,10 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
                         void* greater_col, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    dim3 grid((n + 1 + 127) / 128, p->k_hi - p->k_lo);
-    KBE_LAUNCH("collision_slice_kernel", collision_slice_kernel, grid, dim3(128), 0, stream, *p, (int)n,
-               (cplx*)lesser_row, (cplx*)greater_row, (cplx*)lesser_col, (cplx*)greater_col);
+    KSpec s;
+    make_spec(s, collision_slice_kernel, dim3((n + 1 + 127) / 128, p->k_hi - p->k_lo), dim3(128), 0, *p, (int)n,
+              (cplx*)lesser_row, (cplx*)greater_row, (cplx*)lesser_col, (cplx*)greater_col);
+    KBE_LAUNCH_SPEC("collision_slice_kernel", s);
     return KBE_OK;
 }
 
@@ -1833,13 +2076,19 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
-    return launch_update(p, n, phase, it, stream);
+    if ((rc = ensure_attrs())) return rc;
+    KSpec s;
+    spec_update(s, p, n, phase, it, 0);
+    KBE_LAUNCH_SPEC("update_kernel", s);
+    return KBE_OK;
 }
 
 int kbe_hf_mean(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    KBE_LAUNCH("hf_mean_kernel", hf_mean_kernel, dim3(1), dim3(128), 0, stream, *p, (int)n, (int)phase, (int)it);
+    KSpec s;
+    spec_hf(s, p, n, phase, it);
+    KBE_LAUNCH_SPEC("hf_mean_kernel", s);
     return KBE_OK;
 }
 
@@ -1847,14 +2096,18 @@ int kbe_build_phi(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 1 || n > p->n_steps) { set_err("kbe_build_phi: n", cudaSuccess); return KBE_ERR_ARG; }
-    KBE_LAUNCH("phi_table_kernel", phi_table_kernel, dim3(1), dim3(128), 0, stream, *p, (int)n, (int)n, (int)it, 1);
+    KSpec s;
+    make_spec(s, phi_table_kernel, dim3(1), dim3(128), 0, *p, (int)n, (int)n, (int)it, 1);
+    KBE_LAUNCH_SPEC("phi_table_kernel", s);
     return KBE_OK;
 }
 
 int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    KBE_LAUNCH("finish_kernel", finish_kernel, dim3(1), dim3(256), 0, stream, *p, (int)n);
+    KSpec s;
+    spec_finish(s, p, n);
+    KBE_LAUNCH_SPEC("finish_kernel", s);
     return KBE_OK;
 }
 
@@ -1882,11 +2135,34 @@ int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
 }
 
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream) {
-    (void)use_graph;
-    for (int n = n_first; n <= n_last; ++n) {
-        int rc = kbe_step(p, n, stream);
-        if (rc) return rc;
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n_first < 1 || n_last > p->n_steps) { set_err("kbe_run: n range", cudaSuccess); return KBE_ERR_ARG; }
+    if (!use_graph) {
+        for (int n = n_first; n <= n_last; ++n)
+            if ((rc = kbe_step(p, n, stream))) return rc;
+        return KBE_OK;
     }
+    if (p->front_all || p->front_send) {
+        snprintf(g_err, sizeof(g_err), "kbe_run drives one rank; multi-rank steps are sequenced by the host");
+        return KBE_ERR_ARG;
+    }
+    if ((rc = ensure_attrs())) return rc;
+    StepGraph* sg = nullptr;
+    if (n_first > n_last) return KBE_OK;
+    if ((rc = get_graph(p, n_first, &sg))) return rc;
+    for (int n = n_first; n <= n_last; ++n)
+        if ((rc = graph_step(sg, p, n, stream))) return rc;
+    return KBE_OK;
+}
+
+int kbe_release(const kbe_problem* p) {
+    for (auto& g : g_graphs)
+        if (g && p && g->key.ctl == p->ctl) {
+            cudaDeviceSynchronize();
+            destroy_graph(g);
+            g = nullptr;
+        }
     return KBE_OK;
 }
 

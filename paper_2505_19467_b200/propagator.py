@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -276,6 +277,10 @@ class PropagationDriver:
         self.state = TwoTimeGF(nkl, self.k_lo, capacity, step_cfg.dt, g_hist, frontier=0)
         self.sigma = SigmaHistory(s_hist, capacity)
         self._poisoned = None
+        # one rank: KBE_GRAPH=1 replays kbe_run's step graph (corrector iterations behind
+        # conditional nodes).  Off by default: on B200 the conditional nodes cost more
+        # than the no-op launches they remove (profiles/r01/launch_modes.jsonl).
+        self.use_graph = 1 if os.environ.get("KBE_GRAPH", "0") == "1" else 0
         if self.world > 1:
             self._gather_frontier()
 
@@ -298,7 +303,7 @@ class PropagationDriver:
     def _launch_step(self, n: int) -> None:
         L, P, st = _lib.lib(), self.ws.problem_ptr(), stream_ptr()
         if self.world == 1:
-            _lib.check(L.kbe_step(P, n, st), "kbe_step")
+            _lib.check(L.kbe_run(P, n, n, self.use_graph, st), "kbe_run")
             return
         # k-sharded step: same launch sequence, with one NCCL all-gather of the new
         # G slice after every update (the Sigma input needs all k) and a MAX
@@ -383,7 +388,7 @@ class PropagationDriver:
         self._precheck(n0)
         n1 = min(last, self.capacity)
         if self.world == 1:
-            _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, 0, stream_ptr()), "kbe_run")
+            _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, self.use_graph, stream_ptr()), "kbe_run")
         else:
             for n in range(n0, n1 + 1):
                 self._launch_step(n)
@@ -405,6 +410,14 @@ class PropagationDriver:
 
     def synchronize(self) -> None:
         torch.cuda.current_stream().synchronize()
+
+    def __del__(self):
+        ws = getattr(self, "ws", None)
+        if ws is not None and getattr(self, "use_graph", 0):
+            try:
+                _lib.lib().kbe_release(ws.problem_ptr())
+            except Exception:
+                pass
 
 
 def run(grid: KGrid, model: ModelConfig, step_cfg: StepConfig, schedule: Schedule | None = None,

@@ -255,3 +255,27 @@ def test_large_run_is_deterministic():
     assert [r.iterations for r in ra] == [r.iterations for r in rb]
     assert torch.equal(a.state.hist, b.state.hist)
     assert torch.equal(a.sigma.hist, b.sigma.hist)
+
+
+@pytest.mark.parametrize("name", ["traj_nk4_full.npz", "traj_hf.npz", "traj_langreth.npz", "traj_free.npz"])
+def test_graph_path_equals_stream_path(name, monkeypatch):
+    """kbe_run's step graph (corrector iterations behind conditional nodes) is bitwise
+    identical to the plain stream sequence in which converged iterations are no-ops."""
+    g = load_golden(name)
+    monkeypatch.setenv("KBE_GRAPH", "0")
+    a = _driver_from_fixture(g)
+    assert a.use_graph == 0
+    ra = a.run()
+    monkeypatch.setenv("KBE_GRAPH", "1")
+    b = _driver_from_fixture(g)
+    assert b.use_graph == 1
+    rb = b.run()
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    assert [r.residual_history for r in ra] == [r.residual_history for r in rb]
+    assert torch.equal(a.state.hist, b.state.hist)
+    assert torch.equal(a.sigma.hist, b.sigma.hist)
+    # the same graph replayed after a reset of the history
+    c = _driver_from_fixture(g)
+    rc = [c.step() for _ in range(int(g["n_steps"]))]
+    assert [r.iterations for r in rc] == [r.iterations for r in rb]
+    assert torch.equal(c.state.hist, b.state.hist)
