@@ -18,14 +18,16 @@
  *     (the Python driver allocates them once, at construction).
  *
  * Packed, time-sliced history layout (one per function; G and Sigma):
- *   hist[k_local][ slice_offset(s) + c * plane_len(s) + b ]    complex128
+ *   hist[k_local][ slice_offset(s) + (b/32)*256 + c*32 + b%32 ]    complex128
  *   slice s holds, for b = 0..s, eight complex planes c:
  *     c = 0..3  the LOWER-triangle block X(t_s, t_b)   (row-major 2x2)
  *     c = 4..7  the UPPER-triangle block Y(t_b, t_s)
  *   G:     lower = G<  (advanced along rows),    upper = G>  (along columns)
  *   Sigma: lower = S>  (selfenergy.py:318),      upper = S<  (selfenergy.py:317)
  *   Everything else follows from X(t',t) = -X(t,t')^dagger (state.py:95-109).
- *   plane_len(s) = 8*ceil((s+1)/8) so that every plane starts 128-byte aligned.
+ *   Points are grouped in blocks of 32: one block of one slice (8 planes x 32
+ *   points, 4 KB) is contiguous, so the collision stream moves it with ONE bulk
+ *   copy.  plane_len(s) = 32*ceil((s+1)/32) padded points per plane.
  */
 #ifndef KBE200_H
 #define KBE200_H
@@ -82,8 +84,8 @@ typedef struct kbe_problem {
     void* gc_part;        /* [k_local][nbb][N+1][4]: I> column sums, per point chunk     */
     void* lr_old;         /* [k_local][N+1][4]: I<(t_{n-1}, t_l) kept for the step */
     void* col_old;        /* [k_local][N+1][4]: I>(t_j, t_{n-1}) kept for the step */
-    void* front_send;     /* NULL (1 rank) or [k_local][8][plane_len(N)]            */
-    void* front_all;      /* NULL (1 rank) or [n_k][8][plane_len(N)] (allgathered)  */
+    void* front_send;     /* NULL (1 rank) or [k_local][slice of capacity N layout]  */
+    void* front_all;      /* NULL (1 rank) or [n_k][slice of capacity N] (gathered) */
     void* ctl;            /* kbe_ctl_bytes() of device control state               */
     double* reports;      /* [N+1][KBE_REPORT_W]                                   */
     void* phi;            /* [N+1][k_local][4] complex: Cayley propagator per step */

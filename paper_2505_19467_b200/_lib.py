@@ -20,7 +20,7 @@ TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -117,9 +117,15 @@ def tri_size(n_steps: int) -> int:
 
 
 def plane_len(s: int) -> int:
-    return ((s + 8) // 8) * 8
+    """Padded points per plane of slice s (whole 32-point blocks)."""
+    return (s // 32 + 1) * 32
 
 
 def slice_offset(s: int) -> int:
-    q, r = divmod(s, 8)
-    return 64 * (q + 1) * (4 * q + r)
+    q, r = divmod(s, 32)
+    return 256 * (q + 1) * (16 * q + r)
+
+
+def slice_index(c: int, b: int) -> int:
+    """Element of (plane c, point b) inside a slice: blocks of 8 planes x 32 points."""
+    return (b // 32) * 256 + c * 32 + b % 32

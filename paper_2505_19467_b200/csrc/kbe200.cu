@@ -23,7 +23,7 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 4
+#define KBE_ABI_VERSION 5
 
 typedef double2 cplx;
 
@@ -51,10 +51,17 @@ static void set_err(const char* what, cudaError_t e) {
     } while (0)
 
 // ------------------------------------------------------------------ layout
-__host__ __device__ __forceinline__ int64_t plane_len(int s) { return (int64_t)((s + 8) >> 3) << 3; }
+// Slice s holds points b = 0..s in s/32 + 1 blocks; a block is 8 planes x 32 points
+// (4 KB, contiguous), so one bulk copy moves one block of one slice.
+// plane_len(s) = padded points per plane; sl_idx(c, b) = element (plane c, point b)
+// inside any slice (independent of s).
+__host__ __device__ __forceinline__ int64_t plane_len(int s) { return (int64_t)((s >> 5) + 1) << 5; }
 __host__ __device__ __forceinline__ int64_t slice_off(int s) {
-    const int64_t q = s >> 3, r = s & 7;
-    return 64 * (q + 1) * (4 * q + r);   // 8 planes x sum_{s'<s} plane_len(s')
+    const int64_t q = s >> 5, r = s & 31;
+    return 256 * (q + 1) * (16 * q + r);   // sum_{s'<s} 8 plane_len(s')
+}
+__host__ __device__ __forceinline__ int64_t sl_idx(int c, int b) {
+    return ((int64_t)(b >> 5) << 8) + (c << 5) + (b & 31);
 }
 
 // ------------------------------------------------------------------ complex
@@ -346,14 +353,12 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
 
     // frontier source: [k][8 planes][stride]
     const cplx* src;
-    int64_t kstride, pstride;
+    int64_t kstride;
     if (P.front_all) {
-        src = (const cplx*)P.front_all;
-        pstride = plane_len(P.n_steps);
-        kstride = 8 * pstride;
+        src = (const cplx*)P.front_all;   // one slice-shaped buffer per k, capacity slice
+        kstride = 8 * plane_len(P.n_steps);
     } else {
         src = (const cplx*)P.g_hist + slice_off(n);
-        pstride = plane_len(n);
         kstride = P.tri;
     }
     // stage 0: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
         const int p = i % nhp, c = (i / nhp) & 7, k = i / (nhp * 8);
         const int hp = hp0 + p, b = hp >> 1, comp = hp & 1;
         const int cc = c & 3;
-        const cplx v = __ldg(src + k * kstride + c * pstride + b);
+        const cplx v = __ldg(src + k * kstride + sl_idx(c, b));
         const cplx x = b < n ? cneg(cconj(v)) : v;
         const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
         const bool is_gp = (c < 4) == (comp == 0);
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
         const int k0 = min(P.k_lo + blk * R, nk - R);
         const int lo = P.k_lo + blk * R, hi = min(P.k_lo + (blk + 1) * R, P.k_hi);
         const int plane = comp == 0 ? 4 + jm : jm;
-        cplx* dst = (cplx*)P.s_hist + slice_off(n) + plane * plane_len(n) + b;
+        cplx* dst = (cplx*)P.s_hist + slice_off(n) + sl_idx(plane, b);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int k = k0 + r;
@@ -516,11 +521,13 @@ __global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const 
 #define TB KBE_TILE_B
 #define TS KBE_TILE_S
 
-__device__ __forceinline__ void load_cell(const cplx* base, int64_t pl, int b, cplx* lo, cplx* up) {
+// the 8 planes of point b of one slice (base = slice start)
+__device__ __forceinline__ void load_cell(const cplx* base, int b, cplx* lo, cplx* up) {
+    base += sl_idx(0, b);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) lo[c] = __ldg(base + c * pl + b);
+    for (int c = 0; c < 4; ++c) lo[c] = __ldg(base + 32 * c);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) up[c] = __ldg(base + (4 + c) * pl + b);
+    for (int c = 0; c < 4; ++c) up[c] = __ldg(base + 32 * (4 + c));
 }
 
 // ---- TMA bulk copies + mbarriers (sm_90+ async proxy), one pipeline per warp
@@ -578,7 +585,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // most of the 148 SMs idle).  Column-direction partials are kept per ts-chunk in
 // KBE_COL_CHUNK-granular slots; the consumer (K3) derives the same ts from n.
 // langreth keeps ts = 32.
-#define KBE_COLL_TASKS 4096
+#ifndef KBE_COLL_TASKS
+#define KBE_COLL_TASKS 16384
+#endif
 __host__ __device__ __forceinline__ int coll_tiles(int n, int nkl) {
     const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
     return (T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * nkl;
@@ -591,7 +600,13 @@ __host__ __device__ __forceinline__ int coll_ts(int n, int nkl, int limit_mode) 
     return KBE_COL_CHUNK;
 }
 
+#ifndef KBE_STAGES
 #define KBE_STAGES 3
+#endif
+// timing experiments only (profiles/coll_variants.sh): 1 = no 2x2 products, 2 = no warp reduction
+#ifndef KBE_COLL_EXP
+#define KBE_COLL_EXP 0
+#endif
 // dynamic shared memory of one collision warp-task
 struct CollSmem {
     cplx buf[KBE_STAGES][8][32];   // ring of slice cells: 8 planes x 32 points
@@ -599,16 +614,23 @@ struct CollSmem {
     uint64_t bar[KBE_STAGES];
 };
 
-// Issue the 8 plane copies of history slice s, points [wb0, wb0+32) clipped to the plane.
+// Issue the bulk copy of block wb0/32 of history slice s (wb0 <= s, so the block
+// exists): one 4 KB copy (8 planes x 32 points) off the diagonal; on a diagonal
+// block only the s - wb0 + 1 stored points of each plane are read (8 copies), so
+// the stream moves no padding.
 __device__ __forceinline__ void issue_slice(const cplx* hist, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
                                             uint64_t pol) {
-    const int64_t pl = plane_len(s);
-    const int cnt = (int)min((int64_t)32, pl - wb0);
+    const cplx* src = hist + slice_off(s) + sl_idx(0, wb0);
+    const int cnt = s + 1 - wb0;
+    if (cnt >= 32) {
+        mbar_expect_tx(bar, 8u * 32u * 16u);
+        bulk_g2s(dst[0], src, 8u * 32u * 16u, bar, pol);
+        return;
+    }
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_expect_tx(bar, 8u * bytes);
-    const cplx* base = hist + slice_off(s) + wb0;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], base + c * pl, bytes, bar, pol);
+    for (int c = 0; c < 8; ++c) bulk_g2s(dst[c], src + 32 * c, bytes, bar, pol);
 }
 
 // triangular index t -> (sc, bc) with 0 <= bc <= sc
@@ -618,6 +640,36 @@ __device__ __forceinline__ void tri_decode(int t, int& sc, int& bc) {
     while (s * (s + 1) / 2 > t) --s;
     sc = s;
     bc = t - s * (s + 1) / 2;
+}
+
+// Collision task list: tiles (sc, bc) of the Sigma triangle (part 0, T0 tile rows)
+// and of the G triangle (part 1, T1 rows) for every local k, each split into nsub
+// sub-tiles.  All full off-diagonal tiles come first and the half-full diagonal
+// tiles last, so the dynamic queue ends on short tasks (smaller tail).
+struct CollTask { int kl, part, sc, bc, sub; };
+__device__ __forceinline__ CollTask coll_task(int task, int nkl, int T0, int T1, int nsub) {
+    CollTask t;
+    const int off0 = T0 * (T0 - 1) / 2, off1 = T1 * (T1 - 1) / 2;   // strictly-lower tiles per k
+    const int n_off = (off0 + off1) * nsub * nkl;
+    t.sub = task % nsub;
+    if (task < n_off) {
+        const int q = task / nsub, per = off0 + off1;
+        t.kl = q / per;
+        int r = q % per;
+        t.part = r < off0 ? 0 : 1;
+        if (t.part) r -= off0;
+        int sr, br;
+        tri_decode(r, sr, br);
+        t.sc = sr + 1;
+        t.bc = br;
+    } else {
+        const int q = (task - n_off) / nsub, per = T0 + T1;
+        t.kl = q / per;
+        const int d = q % per;
+        t.part = d < T0 ? 0 : 1;
+        t.sc = t.bc = t.part ? d - T0 : d;
+    }
+    return t;
 }
 
 // One warp = one task of 32 history points x 32 slices; a persistent grid of 1-warp
@@ -652,10 +704,8 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
         const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
         if (task >= total) break;
-        const int kl = task / per_k, r = task % per_k / nsub, sub = task % nsub;
-        const int part = r < tri0 ? 0 : 1;
-        int sc, bc;
-        tri_decode(part == 0 ? r : r - tri0, sc, bc);
+        const CollTask ct = coll_task(task, P.k_hi - P.k_lo, T0, T1, nsub);
+        const int kl = ct.kl, part = ct.part, sc = ct.sc, bc = ct.bc, sub = ct.sub;
         const int smax = part == 0 ? n : n - 1;
         const int s0 = sc * TS + sub * ts, s1 = min(s0 + ts - 1, smax);
         if (s0 > smax) continue;            // empty sub-tile past the frontier
@@ -666,7 +716,6 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
         // frontier slice n (vector) and the streamed triangle
         const cplx* fr = (part == 0 ? G : S) + slice_off(n);
-        const int64_t pln = plane_len(n);
         const cplx* hist = part == 0 ? S : G;
         __syncwarp();
         if (lane == 0)
@@ -682,7 +731,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
                 const int s = s0 + lane;
                 const double w = quad_w(n, s, dt, P.quad);
                 cplx u[4], l[4], a[4];
-                load_cell(fr, pln, s, l, u);
+                load_cell(fr, s, l, u);
                 if (s < n) neg_dag(a, u);
                 else {
 #pragma unroll
@@ -697,7 +746,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
             if (b <= s1) {
                 const double w = quad_w(n, b, dt, P.quad);
                 cplx u[4], l[4];
-                load_cell(fr, pln, b, l, u);
+                load_cell(fr, b, l, u);
                 if (b < n) neg_dag(Ab, u);
                 else {
 #pragma unroll
@@ -717,7 +766,15 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
                 cplx row[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) row[c] = cz();
+#if KBE_COLL_EXP == 1
                 if (b <= s) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) { row[c] = cadd(SL[c], SU[c]); col[c] = cadd(col[c], SL[c]); }
+                }
+                if (false) {
+#else
+                if (b <= s) {
+#endif
                     mm_acc(row, Ab, SU);
                     if (b < s) {
                         mm_bdag_acc(row, Bb, SL);
@@ -736,7 +793,11 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
                 double v[8];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
+#if KBE_COLL_EXP == 2
+                const double rr = v[lane & 7];
+#else
                 const double rr = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
+#endif
                 if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
                 // refill stage st only after every lane has consumed it (WAR across proxies)
                 fence_proxy_async();
@@ -753,7 +814,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
             cplx X[4], Y[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
-            if (b <= s1) load_cell(fr, pln, b, X, Y);
+            if (b <= s1) load_cell(fr, b, X, Y);
             for (int i = 0; i < m; ++i, ++gcount) {
                 const int j = s0 + i;
                 const unsigned st = gcount % KBE_STAGES;
@@ -764,7 +825,15 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
                 cplx acc[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[c] = cz();
+#if KBE_COLL_EXP == 1
                 if (b <= j) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[c] = cadd(GL[c], GU[c]);
+                }
+                if (false) {
+#else
+                if (b <= j) {
+#endif
                     const double w = quad_w(j, b, dt, P.quad);
                     cplx t[4];
                     mm_bdag(t, GL, X);                 // GL X^dag
@@ -782,7 +851,11 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
                 double v[8];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
+#if KBE_COLL_EXP == 2
+                const double rr = v[lane & 7];
+#else
                 const double rr = warp_rs8(v, lane);
+#endif
                 if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)], rr, pol_keep);
                 fence_proxy_async();
                 __syncwarp();
@@ -843,10 +916,8 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
         if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
         const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
         if (task >= total) break;
-        const int kl = task / per_k, r = task % per_k;
-        const int part = r < tri0 ? 0 : 1;
-        int sc, bc;
-        tri_decode(part == 0 ? r : r - tri0, sc, bc);
+        const CollTask ct = coll_task(task, P.k_hi - P.k_lo, T0, T0, 1);   // both triangles run to slice n
+        const int kl = ct.kl, part = ct.part, sc = ct.sc, bc = ct.bc;
         const int s0 = sc * TS, s1 = min(s0 + TS - 1, n);
         const int wb0 = bc * TB;
         const int m = s1 - s0 + 1;
@@ -854,7 +925,6 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
         const cplx* fr = (part == 0 ? G : S) + slice_off(n);
-        const int64_t pln = plane_len(n);
         const cplx* hist = part == 0 ? S : G;
         __syncwarp();
         if (lane == 0)
@@ -867,7 +937,7 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
             const int s = s0 + lane;
             const double w = quad_w(n, s, dt, P.quad);
             cplx l[4], u[4], v[4];
-            load_cell(fr, pln, s, l, u);
+            load_cell(fr, s, l, u);
             if (part == 0) {
                 cplx a[4];
                 if (s < n) neg_dag(a, u);
@@ -897,7 +967,7 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
         for (int c = 0; c < 4; ++c) { P1[c] = cz(); P2[c] = cz(); P3[c] = cz(); colL[c] = cz(); colG[c] = cz(); }
         if (b <= s1) {
             cplx l[4], u[4];
-            load_cell(fr, pln, b, l, u);
+            load_cell(fr, b, l, u);
             wnb = quad_w(n, b, dt, P.quad);
             if (part == 0) {   // P1 = A(b), P2 = B(b), P3 = w(n)_b D(b)
                 if (b < n) neg_dag(P1, u);
@@ -1231,7 +1301,6 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     }
     const int64_t cs = N1 * 4;   // partial chunk stride
     const int cts = coll_ts(nf, nkl, LANG);
-    const int64_t plp = plane_len(n - 1), plc = plane_len(n);
 
     // this thread's (k, point, entry)
     const int c = tid & 3, o = (tid >> 2) % PPC, kl = (tid >> 2) / PPC;
@@ -1253,8 +1322,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         if (own) {
             phr[k] = ph[i * 2 + k];
             phc[k] = ph[j * 2 + k];
-            pgl[k] = prev[(k * 2 + j) * plp + b];
-            pgu[k] = prev[(4 + i * 2 + k) * plp + b];
+            pgl[k] = prev[sl_idx(k * 2 + j, b)];
+            pgu[k] = prev[sl_idx(4 + i * 2 + k, b)];
             if (phase == 1) {
                 olr[k] = lro[k * 2 + j];
                 ocl[k] = clo[i * 2 + k];
@@ -1262,8 +1331,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         }
     }
     if (own && phase == 1) {
-        ol = cur[c * plc + b];
-        ou = cur[(4 + c) * plc + b];
+        ol = cur[sl_idx(c, b)];
+        ou = cur[sl_idx(4 + c, b)];
     }
 
     // ---- phase A: fixed-order partial sums -------------------------------------------
@@ -1378,12 +1447,12 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             fin = fin && isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
         }
         if (b == n - 1) { sRow[kl * 4 + c] = row; sCol[kl * 4 + c] = col; }
-        cur[c * plc + b] = row;
-        cur[(4 + c) * plc + b] = col;
+        cur[sl_idx(c, b)] = row;
+        cur[sl_idx(4 + c, b)] = col;
         if (P.front_send) {
             cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-            fs[c * pm + b] = row;
-            fs[(4 + c) * pm + b] = col;
+            fs[sl_idx(c, b)] = row;
+            fs[sl_idx(4 + c, b)] = col;
         }
     }
     if (diag_cta) {
@@ -1410,7 +1479,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             cplx nl, nu;
             if (phase == 0) {
                 cplx gl[4], gu[4];
-                load_cell(prev, plp, n - 1, gl, gu);
+                load_cell(prev, n - 1, gl, gu);
                 nl = ah(sandwich(gl, dj, dm), sandwich(gl, dm, dj));
                 nu = ah(sandwich(gu, dj, dm), sandwich(gu, dm, dj));
             } else {
@@ -1439,18 +1508,18 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 };
                 nl = ah(dl(dj, dm), dl(dm, dj));
                 nu = ah(dg(dj, dm), dg(dm, dj));
-                const cplx ol = cur[e * plc + n], ou = cur[(4 + e) * plc + n];
+                const cplx ol = cur[sl_idx(e, n)], ou = cur[sl_idx(4 + e, n)];
                 const double d1 = hypot(nl.x - ol.x, nl.y - ol.y), d2 = hypot(nu.x - ou.x, nu.y - ou.y);
                 res = (d1 != d1 || res != res) ? nan : fmax(res, d1);
                 res = (d2 != d2 || res != res) ? nan : fmax(res, d2);
                 fin = fin && isfinite(nl.x) && isfinite(nl.y) && isfinite(nu.x) && isfinite(nu.y);
             }
-            cur[e * plc + n] = nl;
-            cur[(4 + e) * plc + n] = nu;
+            cur[sl_idx(e, n)] = nl;
+            cur[sl_idx(4 + e, n)] = nu;
             if (P.front_send) {
                 cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-                fs[e * pm + n] = nl;
-                fs[(4 + e) * pm + n] = nu;
+                fs[sl_idx(e, n)] = nl;
+                fs[sl_idx(4 + e, n)] = nu;
             }
         }
     }
@@ -1518,13 +1587,12 @@ __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
         for (int kl = 0; kl < nloc; ++kl) {
             const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
             const cplx* a = G + slice_off(n - 1);
-            const int64_t pa = plane_len(n - 1);
             for (int c = 0; c < 4; ++c) {
-                const cplx g0 = a[c * pa + (n - 1)];
+                const cplx g0 = a[sl_idx(c, n - 1)];
                 cplx r = make_double2(g0.y, -g0.x);   // rho = -i G<
                 if (phase == 1) {
                     const cplx* bcur = G + slice_off(n);
-                    const cplx g1 = bcur[c * plane_len(n) + n];
+                    const cplx g1 = bcur[sl_idx(c, n)];
                     r = cscale(cadd(r, make_double2(g1.y, -g1.x)), 0.5);
                 }
                 acc[c] = cadd(acc[c], r);
@@ -1552,9 +1620,8 @@ __global__ void finish_kernel(kbe_problem P, int n) {
     __shared__ double drift[256];
     for (int kl = threadIdx.x; kl < nloc; kl += blockDim.x) {
         const cplx* c = (const cplx*)P.g_hist + (int64_t)kl * P.tri + slice_off(n);
-        const int64_t pl = plane_len(n);
         cplx gl[4], gu[4];
-        for (int i = 0; i < 4; ++i) { gl[i] = c[i * pl + n]; gu[i] = c[(4 + i) * pl + n]; }
+        for (int i = 0; i < 4; ++i) { gl[i] = c[sl_idx(i, n)]; gu[i] = c[sl_idx(4 + i, n)]; }
         double d = 0.0;
         for (int i = 0; i < 4; ++i) {
             cplx t = csub(gu[i], gl[i]);
@@ -1589,13 +1656,13 @@ __global__ void init_slice0_kernel(kbe_problem P) {
     pdl_enter();
     const int kl = blockIdx.x * blockDim.x + threadIdx.x;
     if (kl < P.k_hi - P.k_lo) {
-        cplx* g = (cplx*)P.g_hist + (int64_t)kl * P.tri;   // slice 0: plane_len(0) = 8
-        g[0 * 8] = make_double2(0.0, 1.0);     // G<(0,0)_00 = i
-        g[7 * 8] = make_double2(0.0, -1.0);    // G>(0,0)_11 = -i
+        cplx* g = (cplx*)P.g_hist + (int64_t)kl * P.tri;   // slice 0
+        g[sl_idx(0, 0)] = make_double2(0.0, 1.0);     // G<(0,0)_00 = i
+        g[sl_idx(7, 0)] = make_double2(0.0, -1.0);    // G>(0,0)_11 = -i
         if (P.front_send) {                     // slice 0 of the all-gather send buffer
             const int64_t pm = plane_len(P.n_steps);
             cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-            for (int c = 0; c < 8; ++c) fs[c * pm] = g[c * 8];
+            for (int c = 0; c < 8; ++c) fs[sl_idx(c, 0)] = g[sl_idx(c, 0)];
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1617,11 +1684,11 @@ __global__ void unpack_kernel(const cplx* hist, int64_t tri, int kloc, int N, in
         cplx v = cz();
         if (t <= frontier && tp <= frontier) {
             if (which == 0) {   // lower-stored: X(t,tp) = L(t,tp) for t >= tp
-                if (t >= tp) v = h[slice_off(t) + jm * plane_len(t) + tp];
-                else v = cneg(cconj(h[slice_off(tp) + (m * 2 + j) * plane_len(tp) + t]));
+                if (t >= tp) v = h[slice_off(t) + sl_idx(jm, tp)];
+                else v = cneg(cconj(h[slice_off(tp) + sl_idx(m * 2 + j, t)]));
             } else {            // upper-stored: Y(t,tp) = U(tp,t) for t <= tp
-                if (t <= tp) v = h[slice_off(tp) + (4 + jm) * plane_len(tp) + t];
-                else v = cneg(cconj(h[slice_off(t) + (4 + m * 2 + j) * plane_len(t) + tp]));
+                if (t <= tp) v = h[slice_off(tp) + sl_idx(4 + jm, t)];
+                else v = cneg(cconj(h[slice_off(t) + sl_idx(4 + m * 2 + j, tp)]));
             }
         }
         out[i] = v;
@@ -1642,9 +1709,9 @@ __global__ void pack_kernel(const cplx* lower, const cplx* upper, int kloc, int 
             if (slice_off(mid) <= off) lo = mid; else hi = mid - 1;
         }
         const int s = lo;
-        const int64_t pl = plane_len(s);
-        const int c = (int)((off - slice_off(s)) / pl);
-        const int b = (int)((off - slice_off(s)) % pl);
+        const int64_t o = off - slice_off(s);
+        const int c = (int)((o >> 5) & 7);
+        const int b = (int)(((o >> 8) << 5) + (o & 31));
         cplx v = cz();
         if (b <= s) {
             if (c < 4) v = lower[(((int64_t)kl * 4 + c) * N1 + s) * N1 + b];

@@ -103,10 +103,12 @@ class TwoTimeGF:
 
     # --- frontier slices (device, no host round trip) ----------------------------------
     def slice_view(self, s: int) -> torch.Tensor:
-        """(k_local, 8, s+1) view of slice s: planes 0..3 G<(t_s,t_b), 4..7 G>(t_b,t_s)."""
+        """(k_local, 8, s+1) device copy of slice s: planes 0..3 G<(t_s,t_b), 4..7 G>(t_b,t_s).
+        The slice is stored as blocks of 8 planes x 32 points (include/kbe200.h)."""
         off = _lib.slice_offset(s)
         pl = _lib.plane_len(s)
-        return self.hist[:, off: off + 8 * pl].view(self.n_k_local, 8, pl)[:, :, : s + 1]
+        blk = self.hist[:, off: off + 8 * pl].view(self.n_k_local, pl // 32, 8, 32)
+        return blk.permute(0, 2, 1, 3).reshape(self.n_k_local, 8, pl)[:, :, : s + 1]
 
     @classmethod
     def from_arrays(cls, lesser, greater, dt: float, frontier: int | None = None, k_offset: int = 0):

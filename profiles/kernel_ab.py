@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--n", type=int, default=900)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--random", action="store_true",
+                    help="fill the history with random values instead of propagating to n-1 (timing-only "
+                         "library variants whose results are wrong)")
     args = ap.parse_args()
     cfgw = bench.select_workload(args.workload)
     import paper_2505_19467_b200 as kb
@@ -42,7 +45,12 @@ def main():
     L, P, sp = _lib.lib(), drv.ws.problem_ptr(), stream_ptr()
     st = torch.cuda.current_stream()
     n = args.n
-    _lib.check(L.kbe_run(P, 1, n - 1, 0, sp))
+    if args.random:
+        g = torch.Generator(device="cuda").manual_seed(7)
+        for h in (drv.ws.g_hist, drv.ws.s_hist):
+            torch.view_as_real(h).normal_(0.0, 0.1, generator=g)
+    else:
+        _lib.check(L.kbe_run(P, 1, n - 1, 0, sp))
     _lib.check(L.kbe_sigma_frontier(P, n - 1, 0, sp))
     _lib.check(L.kbe_collision_frontier(P, n - 1, 0, sp))
     _lib.check(L.kbe_update(P, n, 0, 0, sp))
@@ -62,7 +70,8 @@ def main():
         torch.cuda.synchronize()
         return 1e3 * e0.elapsed_time(e1) / args.reps
 
-    out = {"workload": args.workload, "n": n, "env": {k: v for k, v in os.environ.items() if k.startswith("KBE_")}}
+    out = {"workload": args.workload, "n": n, "random": args.random,
+           "env": {k: v for k, v in os.environ.items() if k.startswith("KBE_")}}
     out["collision_us"] = bench_fn(lambda: L.kbe_collision_frontier(P, n, 0, sp))
     out["update_us"] = bench_fn(lambda: L.kbe_update(P, n, 1, 0, sp))
     out["sigma_frontier_us"] = bench_fn(lambda: L.kbe_sigma_frontier(P, n, 0, sp))

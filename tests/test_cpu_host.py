@@ -36,9 +36,14 @@ def test_abi_struct_and_layout():
     acc = 0
     for s in range(300):
         assert L.kbe_slice_offset(s) == acc == _lib.slice_offset(s)
-        assert L.kbe_plane_len(s) % 8 == 0 and L.kbe_plane_len(s) >= s + 1
+        assert L.kbe_plane_len(s) % 32 == 0 and s + 1 <= L.kbe_plane_len(s) <= s + 32
         acc += 8 * L.kbe_plane_len(s)
     assert L.kbe_tri_size(1000) == _lib.slice_offset(1001)
+    # inside a slice: 4 KB blocks of 8 planes x 32 points, every (plane, point) exactly once
+    pl = _lib.plane_len(100)
+    idx = sorted(_lib.slice_index(c, b) for c in range(8) for b in range(pl))
+    assert idx == list(range(8 * pl))
+    assert _lib.slice_index(3, 37) == 256 + 3 * 32 + 5
 
 
 def test_step_tables_match_oracle_model():
