@@ -136,6 +136,14 @@ int kbe_sigma_slice(int32_t n_k, int32_t nb, const void* g_primary, const void* 
  * column sums over the G history triangle (slices 0..n-1). */
 int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream);
 
+/* collision_row (collision.py:141-162): the kernel-level row-slice contraction on
+ * caller buffers (device, complex128, C order): dg_first (n_k,2,2,T1), g_first
+ * (n_k,2,2,T2); s_like, s_other (n_k,2,2,T,P); w1 (T1), w2 (T2) with T1, T2 <= T,
+ * or, when w2_matrix != 0, w2 (T,P) and T2 = T; out (n_k,2,2,P) = term1 + term2. */
+int kbe_collision_row(int32_t n_k, int32_t T, int32_t P, int32_t T1, int32_t T2, int32_t w2_matrix,
+                      const void* dg_first, const void* g_first, const void* s_like, const void* s_other,
+                      const double* w1, const double* w2, void* out, void* stream);
+
 /* Reduce the partials of the last kbe_collision_frontier(n) into the four
  * CollisionSlice arrays (collision.py:165-176), local k, batch-last:
  * lesser_row/greater_row (k_local,2,2,n+1), lesser_col/greater_col (k_local,2,2,n). */

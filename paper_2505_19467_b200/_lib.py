@@ -61,6 +61,7 @@ SIGNATURES = {
     "kbe_sigma_slice": (ctypes.c_int, [_i32, _i32, _p, _p, _p, _p, _i32, _i32, _p, _p, _p, _p, _p, _p]),
     "kbe_collision_frontier": (ctypes.c_int, [_p, _i32, _i32, _p]),
     "kbe_collision_slice": (ctypes.c_int, [_p, _i32, _p, _p, _p, _p, _p]),
+    "kbe_collision_row": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _p, _p, _p, _p, _p, _p, _p, _p]),
     "kbe_update": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_hf_mean": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_build_phi": (ctypes.c_int, [_p, _i32, _i32, _p]),

@@ -70,6 +70,35 @@ def weight_matrix(limits, n_rows: int, dt: float, rule: QuadratureRule) -> np.nd
     return out
 
 
+def collision_row(dg_first, g_first, s_like, s_other, w1, w2) -> np.ndarray:
+    """Row-slice contraction (collision.py:141-162) on the device: ``collision_row_kernel``.
+
+    s_like, s_other: (k,2,2,T,P) over history x pair columns; dg_first: (k,2,2,len(w1));
+    g_first: (k,2,2,len(w2)) for a shared limit, or (k,2,2,T) with a (T,P) per-column
+    w2 -- the reference's einsum shapes.  Returns term1 + term2, shape (k,2,2,P)."""
+    from ._device import as_device_c128, as_device_f64
+    dev = require_cuda()
+    dg, g = as_device_c128(dg_first, dev), as_device_c128(g_first, dev)
+    sl, so = as_device_c128(s_like, dev), as_device_c128(s_other, dev)
+    w1a, w2a = np.asarray(w1, dtype=float).reshape(-1), np.asarray(w2, dtype=float)
+    if sl.dim() != 5 or sl.shape != so.shape or tuple(sl.shape[1:3]) != (2, 2):
+        raise ValueError(f"collision_row: s_like/s_other must be (k,2,2,T,P), got {tuple(sl.shape)} / {tuple(so.shape)}")
+    nk, T, P = int(sl.shape[0]), int(sl.shape[3]), int(sl.shape[4])
+    T1 = int(w1a.shape[0])
+    T2 = T if w2a.ndim == 2 else int(w2a.shape[0])
+    if w2a.ndim == 2 and w2a.shape != (T, P):
+        raise ValueError(f"collision_row: w2 matrix must be {(T, P)}, got {w2a.shape}")
+    if T1 > T or T2 > T or tuple(dg.shape) != (nk, 2, 2, T1) or tuple(g.shape) != (nk, 2, 2, T2):
+        raise ValueError(f"collision_row: operands could not be broadcast together: dg {tuple(dg.shape)}, "
+                         f"g {tuple(g.shape)}, s {tuple(sl.shape)}, w1 ({T1},), w2 {w2a.shape}")
+    w1d, w2d = as_device_f64(w1a, dev), as_device_f64(w2a.reshape(-1), dev)
+    out = torch.empty((nk, 2, 2, P), dtype=torch.complex128, device=dev)
+    _lib.check(_lib.lib().kbe_collision_row(
+        nk, T, P, T1, T2, int(w2a.ndim == 2), dg.data_ptr(), g.data_ptr(), sl.data_ptr(), so.data_ptr(),
+        w1d.data_ptr(), w2d.data_ptr(), out.data_ptr(), stream_ptr()), "kbe_collision_row")
+    return to_host(out)
+
+
 @dataclass
 class CollisionSlice:
     """I components on the step-n frontier (collision.py:165-176)."""

@@ -1166,6 +1166,41 @@ __global__ void collision_slice_kernel(kbe_problem P, int n, cplx* lr, cplx* gr,
     }
 }
 
+// kernel-level collision_row (collision.py:141-162) on caller layouts:
+//   out[k,a,m,l] = sum_{t<T1} w1[t] sum_b dg[k,a,b,t] SL[k,b,m,t,l]
+//                + sum_{t<T2} w2[t | t,l] sum_b g[k,a,b,t] (SL - SO)[k,b,m,t,l]
+// dg: (n_k,2,2,T1); g: (n_k,2,2,T2); SL, SO: (n_k,2,2,T,P); out (n_k,2,2,P) (the t axis of
+// dg / g is the weight length, as in the reference's einsums; a (T,P) w2 has T2 = T).  One thread per (k, m, l)
+// computes both a, so each SL/SO element is read once; consecutive threads walk l
+// (the contiguous axis).  A bench/API helper, not on the step path.
+__global__ void collision_row_kernel(int nk, int T, int P, int T1, int T2, int w2_matrix, const cplx* dg,
+                                     const cplx* g, const cplx* sl, const cplx* so, const double* w1,
+                                     const double* w2, cplx* out) {
+    const int64_t total = (int64_t)nk * 2 * P;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(i % P), m = (int)((i / P) & 1), k = (int)(i / (2 * (int64_t)P));
+        cplx acc[2] = {cz(), cz()};
+        const int tmax = max(T1, T2);
+        for (int t = 0; t < tmax; ++t) {
+            const double a1 = t < T1 ? w1[t] : 0.0;
+            const double a2 = t < T2 ? (w2_matrix ? w2[(int64_t)t * P + l] : w2[t]) : 0.0;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+                const int64_t si = ((((int64_t)k * 2 + b) * 2 + m) * T + t) * P + l;
+                const cplx x = sl[si], d = csub(x, so[si]);
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int64_t ab = ((int64_t)k * 2 + a) * 2 + b;
+                    if (t < T1) acc[a] = cfma(cscale(dg[ab * T1 + t], a1), x, acc[a]);
+                    if (t < T2) acc[a] = cfma(cscale(g[ab * T2 + t], a2), d, acc[a]);
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a) out[(((int64_t)k * 2 + a) * 2 + m) * P + l] = acc[a];
+    }
+}
+
 // =================================================================== K3: update
 // h(k; t_{n-1/2}) (model.py:123-152) and its Cayley propagator (propagator.py:77-94).
 __device__ void build_phi(const kbe_problem& P, const kbe_ctl* ctl, int n, int k, cplx* phi) {
@@ -2136,6 +2171,24 @@ int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void*
     make_spec(s, collision_slice_kernel, dim3((n + 1 + 127) / 128, p->k_hi - p->k_lo), dim3(128), 0, *p, (int)n,
               (cplx*)lesser_row, (cplx*)greater_row, (cplx*)lesser_col, (cplx*)greater_col);
     KBE_LAUNCH_SPEC("collision_slice_kernel", s);
+    return KBE_OK;
+}
+
+int kbe_collision_row(int32_t n_k, int32_t T, int32_t P, int32_t T1, int32_t T2, int32_t w2_matrix,
+                      const void* dg_first, const void* g_first, const void* s_like, const void* s_other,
+                      const double* w1, const double* w2, void* out, void* stream) {
+    if (n_k < 1 || T < 0 || P < 0 || T1 < 0 || T1 > T || T2 < 0 || T2 > T || (w2_matrix && T2 != T) ||
+        !dg_first || !g_first || !s_like || !s_other || !out || (T1 && !w1) || (T2 && !w2)) {
+        set_err("kbe_collision_row", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    const int64_t total = (int64_t)n_k * 2 * P;
+    if (total == 0) return KBE_OK;
+    const int blocks = (int)((total + 127) / 128 < 148 * 32 ? (total + 127) / 128 : 148 * 32);
+    collision_row_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(
+        n_k, T, P, T1, T2, w2_matrix, (const cplx*)dg_first, (const cplx*)g_first, (const cplx*)s_like,
+        (const cplx*)s_other, w1, w2, (cplx*)out);
+    KBE_CHECK_LAUNCH("collision_row_kernel");
     return KBE_OK;
 }
 

@@ -123,3 +123,66 @@ def shard_range(n_k: int, rank: int, world: int) -> tuple[int, int]:
         raise ConfigError(f"n_shards: {world} does not divide n_k={n_k}")
     my = n_k // world
     return rank * my, (rank + 1) * my
+
+
+# ---- fixed-order reducers (engine.py:141-207) ------------------------------------------
+# Host utilities for callers of the reference API.  On the device these orders are
+# realised by the kernels themselves (warp reduce-scatter, fixed chunk order in K3);
+# nothing on the step path calls these functions.
+
+def chunk_partial_sums(terms, block_size: int, axis: int = -1) -> np.ndarray:
+    """Sums over consecutive blocks of ``block_size`` along ``axis`` (engine.py:141-166).
+
+    ceil(m / block_size) chunks, the last one possibly short; each chunk is summed by
+    numpy along the innermost memory axis, so the in-chunk order depends only on the
+    block size."""
+    if block_size < 1:
+        raise ConfigError(f"block_size must be >= 1, got {block_size}")
+    x = np.ascontiguousarray(np.moveaxis(np.asarray(terms), axis, -1))
+    m = x.shape[-1]
+    lead = x.shape[:-1]
+    if m == 0:
+        return np.moveaxis(np.zeros(lead + (0,), dtype=x.dtype), -1, axis)
+    n_full, rest = divmod(m, block_size)
+    pieces = []
+    if n_full:
+        pieces.append(x[..., : n_full * block_size].reshape(lead + (n_full, block_size)).sum(axis=-1))
+    if rest:
+        pieces.append(x[..., n_full * block_size:].sum(axis=-1)[..., None])
+    sums = np.concatenate(pieces, axis=-1) if len(pieces) > 1 else pieces[0]
+    return np.moveaxis(sums, -1, axis)
+
+
+def tree_reduce(parts, axis: int = -1, return_rounds: bool = False):
+    """Offset-doubling pairwise reduction (engine.py:169-191): round r adds element
+    i + 2^r into i for i a multiple of 2^(r+1); ceil(log2 m) rounds."""
+    x = np.moveaxis(np.asarray(parts), axis, -1).copy()
+    m = x.shape[-1]
+    if m == 0:
+        raise ValueError("cannot reduce zero partial sums")
+    stride, rounds = 1, 0
+    while stride < m:
+        src = x[..., stride::2 * stride]
+        x[..., 0: src.shape[-1] * 2 * stride: 2 * stride] += src
+        stride <<= 1
+        rounds += 1
+    total = x[..., 0]
+    return (total, rounds) if return_rounds else total
+
+
+def sequential_reduce(parts, axis: int = -1) -> np.ndarray:
+    """Left-to-right sum of the partials (engine.py:194-202)."""
+    x = np.moveaxis(np.asarray(parts), axis, -1)
+    if x.shape[-1] == 0:
+        raise ValueError("cannot reduce zero partial sums")
+    acc = np.array(x[..., 0], copy=True)
+    for i in range(1, x.shape[-1]):
+        acc += x[..., i]
+    return acc
+
+
+def reduce_partials(parts, schedule: Schedule | None, axis: int = -1) -> np.ndarray:
+    """tree_reduce unless the schedule asks for sequential (engine.py:205-207)."""
+    if schedule is not None and schedule.reduce_mode == "sequential":
+        return sequential_reduce(parts, axis=axis)
+    return tree_reduce(parts, axis=axis)

@@ -203,6 +203,25 @@ def symmetry_residual(state, n: int | None = None) -> float:
     return res
 
 
+def diagonal_blocks(state, n0: int, n1: int) -> tuple[np.ndarray, np.ndarray]:
+    """G<(t_s,t_s) and G>(t_s,t_s) for s = n0..n1, all local k, as host (steps, k, 2, 2)
+    arrays: one device gather over the packed history (no per-step host round trip)."""
+    steps = np.arange(n0, n1 + 1)
+    if not _is_device_state(state):
+        gl = np.moveaxis(state.lesser[:, :, :, steps, steps], -1, 0)
+        gg = np.moveaxis(state.greater[:, :, :, steps, steps], -1, 0)
+        return gl, gg
+    tri = state.hist.shape[1]
+    offs = np.array([_lib.slice_offset(int(t)) for t in steps], dtype=np.int64)
+    blk = (steps // 32) * 256 + steps % 32                      # point s of slice s
+    planes = np.arange(8, dtype=np.int64) * 32
+    idx = (np.arange(state.n_k_local, dtype=np.int64)[None, :, None] * tri
+           + (offs + blk)[:, None, None] + planes[None, None, :])  # (steps, k, 8)
+    vals = torch.take(state.hist, torch.from_numpy(idx).to(state.hist.device))
+    h = to_host(vals)
+    return h[..., 0:4].reshape(len(steps), -1, 2, 2), h[..., 4:8].reshape(len(steps), -1, 2, 2)
+
+
 def observables_at(state, i: int) -> Observables:
     """n_b(k, t_i) = Im G<_bb(k; t_i, t_i) and the density (state.py:125-130)."""
     gl, _ = _diag_blocks(state, i)

@@ -266,8 +266,100 @@ def cfg2_full_fixture():
           ref_seconds=np.array(time.time() - t0))
 
 
+def collision_row_fixture():
+    """collision.collision_row (collision.py:141-162) on random inputs: vector and
+    (T, P) matrix second-term weights, first-term weights shorter than T."""
+    from kbesolve.collision import collision_row
+    rng = np.random.default_rng(41)
+    out = {}
+    for tag, (n_k, T, P) in {"a": (2, 7, 3), "b": (4, 33, 5), "c": (16, 129, 2)}.items():
+        def c(*shape):
+            return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        # the t axis of dg_first / g_first is the weight length (reference einsum shapes)
+        w1 = kb.quadrature_weights(T - 2, 0.02)            # length T-1 < T
+        w2v = kb.quadrature_weights(T - 3, 0.02, "simpson")  # length T-2
+        w2m = rng.uniform(0.0, 0.02, (T, P))
+        dg, gv, gm = c(n_k, 2, 2, T - 1), c(n_k, 2, 2, T - 2), c(n_k, 2, 2, T)
+        sl, so = c(n_k, 2, 2, T, P), c(n_k, 2, 2, T, P)
+        for k, v in dict(dg=dg, gv=gv, gm=gm, sl=sl, so=so, w1=w1, w2v=w2v, w2m=w2m).items():
+            out[f"{k}_{tag}"] = v
+        out[f"vec_{tag}"] = collision_row(dg, gv, sl, so, w1, w2v)
+        out[f"mat_{tag}"] = collision_row(dg, gm, sl, so, w1, w2m)
+    _save("collision_row.npz", **out)
+
+
+def reducers_fixture():
+    """engine.chunk_partial_sums / tree_reduce / sequential_reduce (engine.py:141-202)."""
+    from kbesolve import engine as E
+    rng = np.random.default_rng(43)
+    out = {}
+    for tag, (shape, axis, bs) in {"a": ((3, 1000), -1, 128), "b": ((7, 5, 33), 1, 4), "c": ((300,), 0, 7)}.items():
+        x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        out[f"x_{tag}"] = x
+        out[f"meta_{tag}"] = np.array([axis, bs])
+        out[f"chunks_{tag}"] = E.chunk_partial_sums(x, bs, axis)
+        out[f"tree_{tag}"], rounds = E.tree_reduce(x, axis, return_rounds=True)
+        out[f"rounds_{tag}"] = np.array(rounds)
+        out[f"seq_{tag}"] = E.sequential_reduce(x, axis)
+    _save("reducers.npz", **out)
+
+
+CLI_CONFIG = {"n_k": 4, "dt": 0.02, "n_steps": 30, "u": 1.0, "pulse_intensity": 0.2, "pulse_center": 0.1}
+
+
+def cli_fixture():
+    """`kbesolve run` on a small config: the KBE1 trajectory bytes, the observables and
+    report tables (cli.py:42-87, trajio.py:27-36), and `inspect` output."""
+    import contextlib
+    import io
+    import json
+    import shutil
+    import tempfile
+    from kbesolve import cli
+    d = tempfile.mkdtemp()
+    try:
+        cfg = dict(CLI_CONFIG, trajectory_path=os.path.join(d, "t.kbe"),
+                   observables_path=os.path.join(d, "obs.csv"), report_path=os.path.join(d, "rep.csv"))
+        with open(os.path.join(d, "run.json"), "w") as fh:
+            json.dump(cfg, fh)
+        assert cli.main(["run", "--config", os.path.join(d, "run.json")]) == 0
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert cli.main(["inspect", os.path.join(d, "t.kbe")]) == 0
+        shutil.copy(os.path.join(d, "t.kbe"), os.path.join(HERE, "cli_run.kbe"))
+        shutil.copy(os.path.join(d, "obs.csv"), os.path.join(HERE, "cli_run_observables.csv"))
+        shutil.copy(os.path.join(d, "rep.csv"), os.path.join(HERE, "cli_run_report.csv"))
+        with open(os.path.join(HERE, "cli_run_inspect.txt"), "w") as fh:
+            fh.write(buf.getvalue())
+        with open(os.path.join(HERE, "cli_run_config.json"), "w") as fh:
+            json.dump(CLI_CONFIG, fh, indent=1)
+        print("wrote cli_run.* fixtures")
+    finally:
+        shutil.rmtree(d)
+
+
+def config_fixture():
+    """validate_config (config.py:76-163) on valid and invalid inputs: the exception type
+    and message, or the resolved fields."""
+    import json
+    from kbesolve.config import validate_config
+    cases = json.load(open(os.path.join(HERE, "config_cases.json")))["cases"]
+    results = []
+    for c in cases:
+        try:
+            r = validate_config(c)
+            results.append({"ok": [r.n_k, r.step.dt, r.step.n_steps, r.step.memory_budget, r.step.max_iter,
+                                   r.step.quadrature, r.step.limit_mode, r.schedule.n_shards, r.schedule.workers,
+                                   [r.model.dipole.real, r.model.dipole.imag], r.model.hf_mode, r.seed]})
+        except Exception as e:  # noqa: BLE001
+            results.append({"error": type(e).__name__, "message": str(e)})
+    json.dump({"cases": cases, "results": results}, open(os.path.join(HERE, "config_cases.json"), "w"), indent=0)
+    print(f"wrote config_cases.json ({len(cases)} cases)")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["sigma", "collision", "sigma_batched", "trajectory"]
     for w in which:
         globals()[f"{w}_fixture" if w != "trajectory" else "trajectory_fixtures"]()
+    # also: collision_row, cli, config (python make_golden.py collision_row cli config)
 
