@@ -27,6 +27,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -133,24 +134,48 @@ def cpu_baseline(iterations_per_step=None, budget_s=25.0):
     GPU run's iteration counts (1 + it_n evaluations at step n)."""
     from oracle import kbe_oracle as O
     n_k, N, dt = CFG["n_k"], CFG["n_steps"], CFG["dt"]
-    ns = {2: [100, 200, 300], 16: [100, 200, 300], 32: [50, 100, 150], 64: [20, 40, 60]}.get(n_k, [8, 16, 24])
+    ns = {2: [100, 200, 300], 16: [150, 300, 450], 32: [50, 100, 150], 64: [20, 40, 60]}.get(n_k, [8, 16, 24])
     cap = max(ns)
     drv = O.OracleDriver(n_k, O.Model(u_protocol=1.0), dt, cap)
     GL, GG = O.random_mirrored_state(n_k, cap, cap, seed=3)
     drv.GL[:] = 0.1 * GL
     drv.GG[:] = 0.1 * GG
+    # the reference's own parallel decomposition (selfenergy.py:201, collision.py:264-268):
+    # contiguous k-shards on a thread pool, one per host core up to n_k (numpy releases
+    # the GIL inside the contractions)
+    workers = max(1, min(os.cpu_count() or 1, n_k))
+    shards = [(i * n_k // workers, (i + 1) * n_k // workers) for i in range(workers)]
+    pool = ThreadPoolExecutor(workers)
+
+    def eval_sigma(n):
+        gl_col, gg_row = drv.GL[:, :, :, : n + 1, n], drv.GG[:, :, :, n, : n + 1]
+        U = drv.U
+
+        def one(kr):
+            return (O.sigma_slice(gl_col, gg_row, U[: n + 1], float(U[n]), kr),
+                    O.sigma_slice(gg_row, gl_col, float(U[n]), U[: n + 1], kr))
+        parts = list(pool.map(one, shards))
+        for (k0, k1), (les, gre) in zip(shards, parts):
+            drv.SL[k0:k1, :, :, : n + 1, n] = les
+            drv.SG[k0:k1, :, :, n, : n + 1] = gre
+
+    def eval_collision(n):
+        list(pool.map(lambda kr: O.collision_frontier(drv.GL[kr[0]:kr[1]], drv.GG[kr[0]:kr[1]], drv.SL[kr[0]:kr[1]],
+                                                        drv.SG[kr[0]:kr[1]], n, dt), shards))
+
     ts, tc = [], []
     t_all = time.perf_counter()
     for n in ns:
         t0 = time.perf_counter()
-        drv.eval_sigma(n)
+        eval_sigma(n)
         t1 = time.perf_counter()
-        drv.eval_collision(n)
+        eval_collision(n)
         t2 = time.perf_counter()
         ts.append(t1 - t0)
         tc.append(t2 - t1)
         if time.perf_counter() - t_all > budget_s:
             break
+    pool.shutdown()
     m = len(ts)
     x = np.array(ns[:m], dtype=float)
     bs = np.polyfit(x + 1, ts, 1)
@@ -168,10 +193,11 @@ def cpu_baseline(iterations_per_step=None, budget_s=25.0):
     for n in range(1, N + 1):
         total += sig(n - 1) + col(n - 1) + its[n - 1] * (sig(n) + col(n))
     return {
-        "value": N / total, "unit": "time-steps/s", "cores": 1, "kind": "port",
-        "sample": (f"numpy oracle port, single Sigma+collision evaluations at n={ns[:m]} on a random "
-                   f"n_k={n_k} history ({time.perf_counter() - t_all:.1f}s of CPU), fitted and extrapolated "
-                   f"to the full {N}-step propagation with the measured iteration counts"),
+        "value": N / total, "unit": "time-steps/s", "cores": workers, "kind": "port",
+        "sample": (f"numpy oracle port of the reference, k-sharded over {workers} host threads, single "
+                   f"Sigma+collision evaluations at n={ns[:m]} on a random n_k={n_k} history "
+                   f"({time.perf_counter() - t_all:.1f}s), fitted and extrapolated to the full {N}-step "
+                   f"propagation with the measured iteration counts"),
         "extrapolated_seconds": total,
     }
 
@@ -184,8 +210,15 @@ def _setup_dist(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # KBE_BENCH_SAME_DEVICE=1 + KBE_BENCH_BACKEND=gloo: every rank on cuda:0, for
+        # exercising the sharded path on a one-GPU box (gloo stages through the host)
+        dev = 0 if os.environ.get("KBE_BENCH_SAME_DEVICE") == "1" else local
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("KBE_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return rank, world

@@ -84,8 +84,8 @@ typedef struct kbe_problem {
     void* gc_part;        /* [k_local][nbb][N+1][4]: I> column sums, per point chunk     */
     void* lr_old;         /* [k_local][N+1][4]: I<(t_{n-1}, t_l) kept for the step */
     void* col_old;        /* [k_local][N+1][4]: I>(t_j, t_{n-1}) kept for the step */
-    void* front_send;     /* NULL (1 rank) or [k_local][slice of capacity N layout]  */
-    void* front_all;      /* NULL (1 rank) or [n_k][slice of capacity N] (gathered) */
+    void* front_send;     /* NULL (1 rank) or one all-gather chunk: [k_local][slice of capacity N] + 16-complex control tail */
+    void* front_all;      /* NULL (1 rank) or [ranks][chunk] (gathered)                */
     void* ctl;            /* kbe_ctl_bytes() of device control state               */
     double* reports;      /* [N+1][KBE_REPORT_W]                                   */
     void* phi;            /* [N+1][k_local][4] complex: Cayley propagator per step */

@@ -20,7 +20,8 @@ TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
-ABI_VERSION = 5
+TAIL_CPLX = 16     # per-rank control tail of the all-gather chunk (KBE_TAIL_CPLX)
+ABI_VERSION = 6
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32

@@ -23,7 +23,7 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 5
+#define KBE_ABI_VERSION 6
 
 typedef double2 cplx;
 
@@ -182,10 +182,39 @@ __device__ __forceinline__ double quad_w(int nint, int t, double dt, int quad) {
 }
 
 // ------------------------------------------------------------------ device-side convergence
-__device__ __forceinline__ bool kbe_skip(const kbe_ctl* ctl, int it, double eps) {
+// k-sharded ranks: every rank's all-gather chunk is its new G slice for the local k
+// followed by a 256-byte control tail (its local residual bits and non-finite flags per
+// iteration), so one all-gather per iteration also carries the convergence record and
+// every rank takes the max over ranks itself (no separate all-reduce).
+#define KBE_TAIL_CPLX 16
+struct KbeTail {
+    unsigned long long res[KBE_MAX_ITER];
+    int nonfinite[KBE_MAX_ITER];
+};
+static_assert(sizeof(KbeTail) <= KBE_TAIL_CPLX * sizeof(cplx), "control tail");
+__host__ __device__ __forceinline__ int64_t front_chunk(const kbe_problem& P) {
+    return (int64_t)(P.k_hi - P.k_lo) * 8 * plane_len(P.n_steps) + KBE_TAIL_CPLX;
+}
+__device__ __forceinline__ const KbeTail* rank_tail(const kbe_problem& P, int r) {
+    return (const KbeTail*)((const cplx*)P.front_all + r * front_chunk(P) + front_chunk(P) - KBE_TAIL_CPLX);
+}
+// residual bits / non-finite flag of iteration i over all ranks
+__device__ __forceinline__ unsigned long long res_bits(const kbe_problem& P, const kbe_ctl* ctl, int i) {
+    if (!P.front_all) return ctl->res[i];
+    unsigned long long m = 0;
+    for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) m = max(m, rank_tail(P, r)->res[i]);
+    return m;
+}
+__device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl* ctl, int i) {
+    if (!P.front_all) return ctl->nonfinite[i];
+    int f = 0;
+    for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) f |= rank_tail(P, r)->nonfinite[i];
+    return f;
+}
+__device__ __forceinline__ bool kbe_skip(const kbe_problem& P, const kbe_ctl* ctl, int it) {
     if (ctl->poisoned) return true;
     for (int i = 0; i < it; ++i)
-        if (__longlong_as_double((long long)ctl->res[i]) <= eps) return true;
+        if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) return true;
     return false;
 }
 
@@ -340,7 +369,7 @@ template <int R>
 __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
-    if (kbe_skip(ctl, it, P.eps)) return;
+    if (kbe_skip(P, ctl, it)) return;
     extern __shared__ cplx sm[];
     const int nk = P.n_k;
     const SgDims D(nk);
@@ -352,14 +381,18 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
     const int tid = threadIdx.x;
 
     // frontier source: [k][8 planes][stride]
+    // gathered buffer: rank chunks of [k_local][capacity slice] + control tail
     const cplx* src;
-    int64_t kstride;
+    int64_t kstride, rstride;
+    const int kper = P.front_all ? nloc : nk;
     if (P.front_all) {
-        src = (const cplx*)P.front_all;   // one slice-shaped buffer per k, capacity slice
+        src = (const cplx*)P.front_all;
         kstride = 8 * plane_len(P.n_steps);
+        rstride = front_chunk(P);
     } else {
         src = (const cplx*)P.g_hist + slice_off(n);
         kstride = P.tri;
+        rstride = 0;
     }
     // stage 0: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
     // comp 0: gp = V1, gr = V2;  comp 1: gp = V2, gr = V1 (each half-pair loads both).
@@ -367,7 +400,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
         const int p = i % nhp, c = (i / nhp) & 7, k = i / (nhp * 8);
         const int hp = hp0 + p, b = hp >> 1, comp = hp & 1;
         const int cc = c & 3;
-        const cplx v = __ldg(src + k * kstride + sl_idx(c, b));
+        const cplx v = __ldg(src + (k / kper) * rstride + (k % kper) * kstride + sl_idx(c, b));
         const cplx x = b < n ? cneg(cconj(v)) : v;
         const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
         const bool is_gp = (c < 4) == (comp == 0);
@@ -679,7 +712,7 @@ __device__ __forceinline__ CollTask coll_task(int task, int nkl, int T0, int T1,
 __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (kbe_skip(ctl, it, P.eps)) return;
+    if (kbe_skip(P, ctl, it)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
@@ -893,7 +926,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (kbe_skip(ctl, it, P.eps)) return;
+    if (kbe_skip(P, ctl, it)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
@@ -1307,7 +1340,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
         if (ctl->poisoned) return;
-    } else if (kbe_skip(ctl, it, P.eps)) {
+    } else if (kbe_skip(P, ctl, it)) {
         return;   // graph mode: next_iter keeps its default 0, so the step ends
     }
     const int nkl = P.k_hi - P.k_lo;
@@ -1577,16 +1610,27 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
             atomicMax(&ctl->res[it], bits);
             if (nfl) atomicOr(&ctl->nonfinite[it], 1);
-            if (next_iter) {
-                // graph mode (kbe_run): the last CTA to finish decides whether the next
-                // corrector iteration's conditional body runs (propagator.py:360-368:
-                // continue while residual > eps, NaN included, up to max_iter)
+            if (next_iter || P.front_send) {
+                // the last CTA to finish sees the complete local record:
+                //  - graph mode (kbe_run): decides whether the next corrector iteration's
+                //    conditional body runs (propagator.py:360-368: continue while
+                //    residual > eps, NaN included, up to max_iter);
+                //  - k-sharded: copies the record into this rank's all-gather tail
                 __threadfence();
                 if (atomicAdd(&ctl->upd_done, 1u) == gridDim.x - 1) {
                     ctl->upd_done = 0;
                     __threadfence();
-                    const double rall = __longlong_as_double((long long)atomicOr(&ctl->res[it], 0ull));
-                    if (!(rall <= P.eps)) cudaGraphSetConditional(next_iter, 1u);
+                    if (next_iter) {
+                        const double rall = __longlong_as_double((long long)atomicOr(&ctl->res[it], 0ull));
+                        if (!(rall <= P.eps)) cudaGraphSetConditional(next_iter, 1u);
+                    }
+                    if (P.front_send) {
+                        KbeTail* t = (KbeTail*)((cplx*)P.front_send + front_chunk(P) - KBE_TAIL_CPLX);
+                        for (int i = 0; i < KBE_MAX_ITER; ++i) {
+                            t->res[i] = atomicOr(&ctl->res[i], 0ull);
+                            t->nonfinite[i] = atomicOr(&ctl->nonfinite[i], 0);
+                        }
+                    }
                 }
             }
         }
@@ -1598,7 +1642,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
 __global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int check_skip) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (check_skip && kbe_skip(ctl, it, P.eps)) return;
+    if (check_skip && kbe_skip(P, ctl, it)) return;
     const int nkl = P.k_hi - P.k_lo;
     const int64_t total = (int64_t)(n1 - n0 + 1) * nkl;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1615,7 +1659,7 @@ __global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int chec
 __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(ctl, it, P.eps)) return;
+    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(P, ctl, it)) return;
     const int nloc = P.k_hi - P.k_lo;
     if (threadIdx.x == 0) {
         cplx acc[4] = {cz(), cz(), cz(), cz()};
@@ -1671,19 +1715,20 @@ __global__ void finish_kernel(kbe_problem P, int n) {
     for (int kl = 0; kl < nloc && kl < 256; ++kl) { ds += dens[kl]; dm = fmax(dm, drift[kl]); }
     int iters = P.max_iter, conv = 0;
     for (int i = 0; i < P.max_iter; ++i)
-        if (__longlong_as_double((long long)ctl->res[i]) <= P.eps) { iters = i + 1; conv = 1; break; }
+        if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) { iters = i + 1; conv = 1; break; }
     double* r = P.reports + (int64_t)n * KBE_REPORT_W;
+    const int nonfin = nonfinite_at(P, ctl, iters - 1);
     r[0] = n;
     r[1] = iters;
-    r[2] = __longlong_as_double((long long)ctl->res[iters - 1]);
+    r[2] = __longlong_as_double((long long)res_bits(P, ctl, iters - 1));
     r[3] = conv;
     r[4] = dm;
     r[5] = ds;
-    r[6] = ctl->nonfinite[iters - 1];
+    r[6] = nonfin;
     r[7] = 0.0;
     for (int i = 0; i < KBE_MAX_ITER; ++i)
-        r[8 + i] = i < iters ? __longlong_as_double((long long)ctl->res[i]) : 0.0;
-    if (ctl->nonfinite[iters - 1]) ctl->poisoned = n;
+        r[8 + i] = i < iters ? __longlong_as_double((long long)res_bits(P, ctl, i)) : 0.0;
+    if (nonfin) ctl->poisoned = n;
 }
 
 // =================================================================== init / pack / unpack

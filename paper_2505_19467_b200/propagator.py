@@ -176,9 +176,11 @@ class _Workspace:
         self.amp = as_device_f64(amp, device)
         self.front_send = self.front_all = None
         if multi_rank:
-            pm = _lib.plane_len(n_steps)
-            self.front_send = torch.zeros((kl, 8, pm), **c128)
-            self.front_all = torch.zeros((n_k, 8, pm), **c128)
+            # one all-gather chunk per rank: [k_local][capacity slice] + control tail
+            # (residual bits and non-finite flags; include/kbe200.h)
+            chunk = kl * 8 * _lib.plane_len(n_steps) + _lib.TAIL_CPLX
+            self.front_send = torch.zeros(chunk, **c128)
+            self.front_all = torch.zeros((n_k // kl, chunk), **c128)
         p = _lib.KbeProblem()
         p.n_k, p.k_lo, p.k_hi, p.n_steps = n_k, k_lo, k_hi, n_steps
         p.quad, p.limit_mode, p.hf, p.max_iter = quad, limit_mode, int(hf), max_iter
@@ -289,12 +291,6 @@ class PropagationDriver:
         """All-gather the new G slice (local k) into the all-k frontier buffer."""
         all_gather_device(self.ws.front_all, self.ws.front_send)
 
-    def _allreduce_ctl(self, it: int) -> None:
-        """Global max of residual bits and non-finite flags (same decision on every rank)."""
-        import torch.distributed as dist
-        all_reduce_device(self.ws.ctl[: 8 * _lib.MAX_ITER].view(torch.int64), dist.ReduceOp.MAX)
-        all_reduce_device(self.ws.ctl[8 * _lib.MAX_ITER: 12 * _lib.MAX_ITER].view(torch.int32), dist.ReduceOp.MAX)
-
     def _allreduce_hf(self) -> None:
         import torch.distributed as dist
         off = 208   # offsetof(kbe_ctl, hf_sum): 128 res + 64 nonfinite + 8 poisoned/pad, 16-aligned
@@ -305,9 +301,9 @@ class PropagationDriver:
         if self.world == 1:
             _lib.check(L.kbe_run(P, n, n, self.use_graph, st), "kbe_run")
             return
-        # k-sharded step: same launch sequence, with one NCCL all-gather of the new
-        # G slice after every update (the Sigma input needs all k) and a MAX
-        # all-reduce of the convergence record.
+        # k-sharded step: same launch sequence, with one NCCL all-gather after every
+        # update.  It carries the new G slice (the Sigma input needs all k) and each
+        # rank's convergence record, which every kernel max-reduces over ranks itself.
         chk = _lib.check
         nold = n - 1
         if self.interactions_on:
@@ -328,7 +324,6 @@ class PropagationDriver:
                 self._allreduce_hf()
                 chk(L.kbe_build_phi(P, n, it, st), "kbe_build_phi")
             chk(L.kbe_update(P, n, 1, it, st), "kbe_update")
-            self._allreduce_ctl(it)
             self._gather_frontier()
         chk(L.kbe_finish_step(P, n, st), "kbe_finish_step")
 

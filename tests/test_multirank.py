@@ -40,16 +40,18 @@ def test_collectives_world2_gloo(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("hf", ["off", "on"])
-def test_k_sharded_driver_matches_single_rank(tmp_path, hf):
+@pytest.mark.parametrize("hf, world", [("off", 2), ("on", 2), ("off", 4)])
+def test_k_sharded_driver_matches_single_rank(tmp_path, hf, world):
+    """Each all-gather chunk carries the rank's G slice and its convergence record; the
+    kernels max-reduce the records over ranks, so iteration counts match exactly."""
     import paper_2505_19467_b200 as kb
     n_k, n_steps = 8, 40
     os.environ["KBE_HF"] = hf
     try:
-        mp.spawn(W.driver_worker, args=(2, _port(), str(tmp_path), n_k, n_steps), nprocs=2, join=True)
+        mp.spawn(W.driver_worker, args=(world, _port(), str(tmp_path), n_k, n_steps), nprocs=world, join=True)
     finally:
         os.environ.pop("KBE_HF", None)
-    parts = [np.load(tmp_path / f"drv{r}.npz") for r in (0, 1)]
+    parts = [np.load(tmp_path / f"drv{r}.npz") for r in range(world)]
     hist = np.concatenate([p["hist"] for p in parts])
     sig = np.concatenate([p["sig"] for p in parts])
     torch.cuda.set_device(0)
