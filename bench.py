@@ -253,7 +253,7 @@ def _reset(kb, drv):
     drv.state.frontier = 0
     drv._poisoned = None
     if drv.world > 1:
-        drv._gather_frontier()
+        drv.publish_initial()
 
 
 def _collision_roofline(kb, drv, hbm_peak):
@@ -417,6 +417,7 @@ def run_ours(args):
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
+        drv.close()
         dist.destroy_process_group()
 
 

@@ -44,6 +44,7 @@ extern "C" {
 #define KBE_ERR_UNSUPPORTED 3
 
 #define KBE_MAX_ITER 16      /* StepConfig.max_iter ceiling on the device path */
+#define KBE_MAX_RANKS 8      /* k-shard ranks of one NVLink/NVSwitch domain (peer-to-peer exchange) */
 #define KBE_TILE_B 32        /* collision warp-task: history points            */
 #define KBE_TILE_S 32        /* collision tile: time slices (a warp task takes 8, 16 or 32 of them) */
 #define KBE_COL_CHUNK 8      /* column-direction partial slots: one per 8 slices */
@@ -96,6 +97,13 @@ typedef struct kbe_problem {
     void* lc_part;        /* [k_local][nbb][N+1][4]: I< column, row-direction sums  */
     void* gc_part_c;      /* [k_local][nsb][N+1][4]: I> column, column-direction    */
     void* lc_part_c;      /* [k_local][nsb][N+1][4]: I< column, column-direction    */
+    /* peer-to-peer exchange over NVLink (p2p_world > 1; front_send / front_all are
+     * then unused except for the initial slice): every rank owns a kbe_p2p_bytes()
+     * buffer, opened by every peer through kbe_p2p_export / kbe_p2p_open. */
+    int32_t p2p_world;    /* ranks exchanging through peer memory (0/1: off)       */
+    int32_t p2p_rank;
+    void* p2p_local;      /* this rank's buffer                                    */
+    void* p2p_peers[KBE_MAX_RANKS];  /* every rank's buffer as mapped here (incl. self) */
 } kbe_problem;
 
 /* ---- layout helpers (host-callable, no device work) ---------------------- */
@@ -189,6 +197,22 @@ int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_g
 
 /* Drop the step graph cached for this problem's control block (driver teardown). */
 int kbe_release(const kbe_problem* p);
+
+/* ---- peer-to-peer frontier exchange (k-sharded ranks) ---------------
+ * Replaces the per-iteration NCCL all-gather (propagator.py's _gather_frontier) by
+ * stores from the update kernel into every peer's buffer over NVLink plus epoch
+ * flags.  Buffer = [2 parities][world][chunk complex] + world flags + epoch, where
+ * chunk = k_local * 8 * plane_len(N) + 16 (slice + control tail). */
+int64_t kbe_p2p_bytes(const kbe_problem* p, int32_t world);
+/* cudaMalloc + zero a buffer and export its IPC handle (64 bytes) for the peers. */
+int kbe_p2p_alloc(int64_t bytes, void** ptr_out, void* ipc_handle_out);
+/* Map a peer's buffer from its IPC handle (cudaIpcOpenMemHandle); close with kbe_p2p_close. */
+int kbe_p2p_open(const void* ipc_handle, void** ptr_out);
+int kbe_p2p_close(void* ptr);
+int kbe_p2p_free(void* ptr);
+/* Publish this rank's send chunk (front_send: the initial slice) to every peer at the
+ * next epoch; used after kbe_init_history instead of the NCCL all-gather. */
+int kbe_p2p_publish(const kbe_problem* p, void* stream);
 
 /* ---- layout conversion (TwoTimeGF / SigmaHistory accessors) -------------- */
 /* Rebuild the reference layout (k_local,2,2,N+1,N+1) of one function from the

@@ -16,12 +16,13 @@ LIB_PATH = os.environ.get("KBE_LIB") or os.environ.get("KBE200_LIB", os.path.joi
 
 KBE_OK, KBE_ERR_ARG, KBE_ERR_CUDA, KBE_ERR_UNSUPPORTED = 0, 1, 2, 3
 MAX_ITER = 16
+MAX_RANKS = 8
 TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
 TAIL_CPLX = 16     # per-rank control tail of the all-gather chunk (KBE_TAIL_CPLX)
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -45,6 +46,7 @@ class KbeProblem(ctypes.Structure):
         ("front_send", _p), ("front_all", _p),
         ("ctl", _p), ("reports", _p), ("phi", _p),
         ("row_part_g", _p), ("col_part_g", _p), ("lc_part", _p), ("gc_part_c", _p), ("lc_part_c", _p),
+        ("p2p_world", _i32), ("p2p_rank", _i32), ("p2p_local", _p), ("p2p_peers", _p * 8),
     ]
 
 
@@ -70,6 +72,12 @@ SIGNATURES = {
     "kbe_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_run": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_release": (ctypes.c_int, [_p]),
+    "kbe_p2p_bytes": (_i64, [_p, _i32]),
+    "kbe_p2p_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(_p), _p]),
+    "kbe_p2p_open": (ctypes.c_int, [_p, ctypes.POINTER(_p)]),
+    "kbe_p2p_close": (ctypes.c_int, [_p]),
+    "kbe_p2p_free": (ctypes.c_int, [_p]),
+    "kbe_p2p_publish": (ctypes.c_int, [_p, _p]),
     "kbe_unpack": (ctypes.c_int, [_p, _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "kbe_pack": (ctypes.c_int, [_p, _p, _i32, _i32, _i32, _i64, _p, _p]),
 }

@@ -23,7 +23,7 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 6
+#define KBE_ABI_VERSION 7
 
 typedef double2 cplx;
 
@@ -195,18 +195,69 @@ static_assert(sizeof(KbeTail) <= KBE_TAIL_CPLX * sizeof(cplx), "control tail");
 __host__ __device__ __forceinline__ int64_t front_chunk(const kbe_problem& P) {
     return (int64_t)(P.k_hi - P.k_lo) * 8 * plane_len(P.n_steps) + KBE_TAIL_CPLX;
 }
+// Peer-to-peer exchange (p2p_world > 1, kbe_p2p_* in include/kbe200.h): every rank owns
+// one buffer [2 parities][ranks][chunk] + flags[ranks] + epoch.  The update kernel
+// writes its new slice and control tail straight into every peer's buffer over
+// NVLink (parity of the next data epoch), and its last CTA bumps the local epoch and
+// release-stores it into flags[me] of every peer.  A consumer waits until all flags
+// reach its local epoch (acquire) and reads the chunks of that epoch's parity.
+// Double buffering makes the overwrite safe: a rank publishes epoch e+1 only after
+// its Sigma waited for every rank's epoch e, i.e. after every rank finished reading
+// epoch e-1 (same parity).
+__host__ __device__ __forceinline__ bool sharded(const kbe_problem& P) { return P.front_all || P.p2p_world > 1; }
+__device__ __forceinline__ unsigned long long* p2p_flags(const kbe_problem& P, void* base) {
+    return (unsigned long long*)((cplx*)base + 2 * (int64_t)P.p2p_world * front_chunk(P));
+}
+__device__ __forceinline__ unsigned long long p2p_epoch(const kbe_problem& P) {
+    return *(volatile unsigned long long*)(p2p_flags(P, P.p2p_local) + P.p2p_world);
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// chunks of the current data epoch (gathered by NCCL, or by peers' stores)
+__device__ __forceinline__ const cplx* front_base(const kbe_problem& P) {
+    if (P.p2p_world > 1)
+        return (const cplx*)P.p2p_local + (int64_t)(p2p_epoch(P) & 1) * P.p2p_world * front_chunk(P);
+    return (const cplx*)P.front_all;
+}
+// where rank `me` writes its chunk in peer r's buffer for data epoch e
+__device__ __forceinline__ cplx* p2p_dst(const kbe_problem& P, int r, unsigned long long e) {
+    return (cplx*)P.p2p_peers[r] + ((int64_t)(e & 1) * P.p2p_world + P.p2p_rank) * front_chunk(P);
+}
+// consumer side: block until every rank has published the local epoch
+__device__ __forceinline__ void p2p_wait(const kbe_problem& P) {
+    if (P.p2p_world <= 1) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long e = p2p_epoch(P);
+        const unsigned long long* f = p2p_flags(P, P.p2p_local);
+        for (int r = 0; r < P.p2p_world; ++r)
+            while (ld_acquire_sys(f + r) < e) __nanosleep(64);
+    }
+    __syncthreads();
+}
+// producer side (one thread, after every CTA's stores were fenced): epoch + 1 everywhere
+__device__ __forceinline__ void p2p_signal(const kbe_problem& P, unsigned long long e) {
+    __threadfence_system();
+    *(volatile unsigned long long*)(p2p_flags(P, P.p2p_local) + P.p2p_world) = e;
+    for (int r = 0; r < P.p2p_world; ++r) st_release_sys(p2p_flags(P, P.p2p_peers[r]) + P.p2p_rank, e);
+}
 __device__ __forceinline__ const KbeTail* rank_tail(const kbe_problem& P, int r) {
-    return (const KbeTail*)((const cplx*)P.front_all + r * front_chunk(P) + front_chunk(P) - KBE_TAIL_CPLX);
+    return (const KbeTail*)(front_base(P) + r * front_chunk(P) + front_chunk(P) - KBE_TAIL_CPLX);
 }
 // residual bits / non-finite flag of iteration i over all ranks
 __device__ __forceinline__ unsigned long long res_bits(const kbe_problem& P, const kbe_ctl* ctl, int i) {
-    if (!P.front_all) return ctl->res[i];
+    if (!sharded(P)) return ctl->res[i];
     unsigned long long m = 0;
     for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) m = max(m, rank_tail(P, r)->res[i]);
     return m;
 }
 __device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl* ctl, int i) {
-    if (!P.front_all) return ctl->nonfinite[i];
+    if (!sharded(P)) return ctl->nonfinite[i];
     int f = 0;
     for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) f |= rank_tail(P, r)->nonfinite[i];
     return f;
@@ -369,6 +420,7 @@ template <int R>
 __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
     if (kbe_skip(P, ctl, it)) return;
     extern __shared__ cplx sm[];
     const int nk = P.n_k;
@@ -384,9 +436,9 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
     // gathered buffer: rank chunks of [k_local][capacity slice] + control tail
     const cplx* src;
     int64_t kstride, rstride;
-    const int kper = P.front_all ? nloc : nk;
-    if (P.front_all) {
-        src = (const cplx*)P.front_all;
+    const int kper = sharded(P) ? nloc : nk;
+    if (sharded(P)) {
+        src = front_base(P);
         kstride = 8 * plane_len(P.n_steps);
         rstride = front_chunk(P);
     } else {
@@ -712,6 +764,7 @@ __device__ __forceinline__ CollTask coll_task(int task, int nkl, int T0, int T1,
 __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
     if (kbe_skip(P, ctl, it)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
@@ -926,6 +979,7 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
     if (kbe_skip(P, ctl, it)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
@@ -1333,6 +1387,28 @@ static size_t upd_smem_bytes(int nkl, int ppc) {
                            + (size_t)6 * nkl * 4);            // sC, sRow, sCol, sX, sY, sZ
 }
 
+// k-sharded publication of one frontier entry (plane c, point b) of local k kl:
+// the NCCL send buffer, or straight into every peer's buffer for data epoch e
+__device__ __forceinline__ void publish_entry(const kbe_problem& P, int kl, int c, int b, cplx v, int64_t pm,
+                                              unsigned long long e) {
+    const int64_t off = (int64_t)kl * 8 * pm + sl_idx(c, b);
+    if (P.p2p_world > 1) {
+        for (int r = 0; r < P.p2p_world; ++r) p2p_dst(P, r, e)[off] = v;
+    } else if (P.front_send) {
+        ((cplx*)P.front_send)[off] = v;
+    }
+}
+// control tail of this rank (one thread); P2P: then bump the epoch on every rank
+__device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail& t, unsigned long long e) {
+    const int64_t off = front_chunk(P) - KBE_TAIL_CPLX;
+    if (P.p2p_world > 1) {
+        for (int r = 0; r < P.p2p_world; ++r) *(KbeTail*)(p2p_dst(P, r, e) + off) = t;
+        p2p_signal(P, e);
+    } else if (P.front_send) {
+        *(KbeTail*)((cplx*)P.front_send + off) = t;
+    }
+}
+
 template <int LANG>
 __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC,
                                                      cudaGraphConditionalHandle next_iter) {
@@ -1482,7 +1558,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     __syncthreads();
 
     // ---- phase B: row / column update of the own points ----------------------------------
-    const int64_t pm = P.front_send ? plane_len(P.n_steps) : 0;
+    const int64_t pm = sharded(P) ? plane_len(P.n_steps) : 0;
+    const unsigned long long e_next = P.p2p_world > 1 ? p2p_epoch(P) + 1 : 0;   // data epoch this update publishes
     double res = 0.0;
     bool fin = true;
     if (own) {
@@ -1517,11 +1594,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         if (b == n - 1) { sRow[kl * 4 + c] = row; sCol[kl * 4 + c] = col; }
         cur[sl_idx(c, b)] = row;
         cur[sl_idx(4 + c, b)] = col;
-        if (P.front_send) {
-            cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-            fs[sl_idx(c, b)] = row;
-            fs[sl_idx(4 + c, b)] = col;
-        }
+        publish_entry(P, kl, c, b, row, pm, e_next);
+        publish_entry(P, kl, 4 + c, b, col, pm, e_next);
     }
     if (diag_cta) {
         __syncthreads();   // sRow / sCol of point n-1
@@ -1584,11 +1658,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             }
             cur[sl_idx(e, n)] = nl;
             cur[sl_idx(4 + e, n)] = nu;
-            if (P.front_send) {
-                cplx* fs = (cplx*)P.front_send + (int64_t)kl * 8 * pm;
-                fs[sl_idx(e, n)] = nl;
-                fs[sl_idx(4 + e, n)] = nu;
-            }
+            publish_entry(P, kl, e, n, nl, pm, e_next);
+            publish_entry(P, kl, 4 + e, n, nu, pm, e_next);
         }
     }
     if (phase == 1) {
@@ -1610,32 +1681,37 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             const unsigned long long bits = (r != r) ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(r);
             atomicMax(&ctl->res[it], bits);
             if (nfl) atomicOr(&ctl->nonfinite[it], 1);
-            if (next_iter || P.front_send) {
-                // the last CTA to finish sees the complete local record:
-                //  - graph mode (kbe_run): decides whether the next corrector iteration's
-                //    conditional body runs (propagator.py:360-368: continue while
-                //    residual > eps, NaN included, up to max_iter);
-                //  - k-sharded: copies the record into this rank's all-gather tail
+        }
+    }
+    if (next_iter || sharded(P)) {
+        // the last CTA to finish sees the complete local record:
+        //  - graph mode (kbe_run): decides whether the next corrector iteration's
+        //    conditional body runs (propagator.py:360-368: continue while
+        //    residual > eps, NaN included, up to max_iter);
+        //  - k-sharded: publishes the record as this rank's control tail (NCCL send
+        //    buffer, or every peer's buffer + the epoch flags)
+        if (P.p2p_world > 1) __threadfence_system();   // this thread's peer stores
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            if (atomicAdd(&ctl->upd_done, 1u) == gridDim.x - 1) {
+                ctl->upd_done = 0;
                 __threadfence();
-                if (atomicAdd(&ctl->upd_done, 1u) == gridDim.x - 1) {
-                    ctl->upd_done = 0;
-                    __threadfence();
-                    if (next_iter) {
-                        const double rall = __longlong_as_double((long long)atomicOr(&ctl->res[it], 0ull));
-                        if (!(rall <= P.eps)) cudaGraphSetConditional(next_iter, 1u);
+                if (next_iter && phase == 1) {
+                    const double rall = __longlong_as_double((long long)atomicOr(&ctl->res[it], 0ull));
+                    if (!(rall <= P.eps)) cudaGraphSetConditional(next_iter, 1u);
+                }
+                if (sharded(P)) {
+                    KbeTail t;
+                    for (int i = 0; i < KBE_MAX_ITER; ++i) {
+                        t.res[i] = atomicOr(&ctl->res[i], 0ull);
+                        t.nonfinite[i] = atomicOr(&ctl->nonfinite[i], 0);
                     }
-                    if (P.front_send) {
-                        KbeTail* t = (KbeTail*)((cplx*)P.front_send + front_chunk(P) - KBE_TAIL_CPLX);
-                        for (int i = 0; i < KBE_MAX_ITER; ++i) {
-                            t->res[i] = atomicOr(&ctl->res[i], 0ull);
-                            t->nonfinite[i] = atomicOr(&ctl->nonfinite[i], 0);
-                        }
-                    }
+                    publish_tail(P, t, e_next);
                 }
             }
         }
     }
-
 }
 
 // Phi(t_{n-1/2}, k) for steps n in [n0, n1], local k (hf term from ctl->hf_sum when hf_mode="on")
@@ -1692,6 +1768,7 @@ __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
 // =================================================================== K4: finish
 __global__ void finish_kernel(kbe_problem P, int n) {
     pdl_enter();
+    p2p_wait(P);
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (ctl->poisoned) return;
     const int nloc = P.k_hi - P.k_lo;
@@ -1729,6 +1806,26 @@ __global__ void finish_kernel(kbe_problem P, int n) {
     for (int i = 0; i < KBE_MAX_ITER; ++i)
         r[8 + i] = i < iters ? __longlong_as_double((long long)res_bits(P, ctl, i)) : 0.0;
     if (nonfin) ctl->poisoned = n;
+}
+
+// Initial slice to every peer (kbe_p2p_publish): copy front_send's chunk into every
+// peer's buffer at the next epoch, then the last CTA signals.
+__global__ void p2p_publish_kernel(kbe_problem P) {
+    pdl_enter();
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    const unsigned long long e = p2p_epoch(P) + 1;
+    const int64_t chunk = front_chunk(P);
+    const cplx* src = (const cplx*)P.front_send;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunk; i += (int64_t)gridDim.x * blockDim.x) {
+        const cplx v = src[i];
+        for (int r = 0; r < P.p2p_world; ++r) p2p_dst(P, r, e)[i] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&ctl->upd_done, 1u) == gridDim.x - 1) {
+        ctl->upd_done = 0;
+        p2p_signal(P, e);
+    }
 }
 
 // =================================================================== init / pack / unpack
@@ -1919,6 +2016,12 @@ static int check_problem(const kbe_problem* p) {
         return KBE_ERR_UNSUPPORTED;
     }
     if (!p->phi) { set_err("kbe_problem.phi", cudaSuccess); return KBE_ERR_ARG; }
+    if (p->p2p_world > 1 && (p->p2p_world > KBE_MAX_RANKS || !p->p2p_local || p->p2p_rank < 0 ||
+                             p->p2p_rank >= p->p2p_world || p->n_k % p->p2p_world ||
+                             (p->k_hi - p->k_lo) * p->p2p_world != p->n_k)) {
+        snprintf(g_err, sizeof(g_err), "kbe_problem: inconsistent peer-to-peer rank set");
+        return KBE_ERR_ARG;
+    }
     return KBE_OK;
 }
 
@@ -2167,7 +2270,7 @@ int kbe_sigma_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_sigma_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
-    if (!p->front_all && (p->k_lo != 0 || p->k_hi != p->n_k)) {
+    if (!sharded(*p) && (p->k_lo != 0 || p->k_hi != p->n_k)) {
         snprintf(g_err, sizeof(g_err), "kbe_sigma_frontier: a k-sharded rank needs the gathered frontier (front_all)");
         return KBE_ERR_ARG;
     }
@@ -2279,7 +2382,7 @@ int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
 int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    if (p->front_all || p->front_send) {
+    if (sharded(*p) || p->front_send) {
         snprintf(g_err, sizeof(g_err), "kbe_step drives one rank; multi-rank steps are sequenced by the host");
         return KBE_ERR_ARG;
     }
@@ -2308,7 +2411,7 @@ int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_g
             if ((rc = kbe_step(p, n, stream))) return rc;
         return KBE_OK;
     }
-    if (p->front_all || p->front_send) {
+    if (sharded(*p) || p->front_send) {
         snprintf(g_err, sizeof(g_err), "kbe_run drives one rank; multi-rank steps are sequenced by the host");
         return KBE_ERR_ARG;
     }
@@ -2355,6 +2458,54 @@ int kbe_pack(const void* lower_full, const void* upper_full, int32_t k_local, in
     pack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const cplx*)lower_full, (const cplx*)upper_full,
                                                                k_local, n_steps, frontier, tri, (cplx*)hist);
     KBE_CHECK_LAUNCH("pack_kernel");
+    return KBE_OK;
+}
+
+int64_t kbe_p2p_bytes(const kbe_problem* p, int32_t world) {
+    if (!p || world < 1) return -1;
+    return (int64_t)2 * world * front_chunk(*p) * (int64_t)sizeof(cplx) + 8 * (int64_t)(world + 2);
+}
+
+int kbe_p2p_alloc(int64_t bytes, void** ptr_out, void* ipc_handle_out) {
+    if (bytes <= 0 || !ptr_out || !ipc_handle_out) { set_err("kbe_p2p_alloc", cudaSuccess); return KBE_ERR_ARG; }
+    cudaError_t e = cudaMalloc(ptr_out, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemset(*ptr_out, 0, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle((cudaIpcMemHandle_t*)ipc_handle_out, *ptr_out);
+    if (e != cudaSuccess) { set_err("kbe_p2p_alloc", e); return KBE_ERR_CUDA; }
+    return KBE_OK;
+}
+
+int kbe_p2p_open(const void* ipc_handle, void** ptr_out) {
+    if (!ipc_handle || !ptr_out) { set_err("kbe_p2p_open", cudaSuccess); return KBE_ERR_ARG; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) { set_err("kbe_p2p_open", e); return KBE_ERR_CUDA; }
+    return KBE_OK;
+}
+
+int kbe_p2p_close(void* ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) { set_err("kbe_p2p_close", e); return KBE_ERR_CUDA; }
+    return KBE_OK;
+}
+
+int kbe_p2p_free(void* ptr) {
+    cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) { set_err("kbe_p2p_free", e); return KBE_ERR_CUDA; }
+    return KBE_OK;
+}
+
+int kbe_p2p_publish(const kbe_problem* p, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (p->p2p_world < 2 || p->p2p_world > KBE_MAX_RANKS || !p->p2p_local || !p->front_send) {
+        set_err("kbe_p2p_publish", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    KSpec s;
+    make_spec(s, p2p_publish_kernel, dim3(64), dim3(256), 0, *p);
+    KBE_LAUNCH_SPEC("p2p_publish_kernel", s);
     return KBE_OK;
 }
 

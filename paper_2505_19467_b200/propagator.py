@@ -225,6 +225,68 @@ class _Workspace:
                    g_hist=state.hist, s_hist=sigma.hist, device=state.hist.device)
 
 
+class _PeerExchange:
+    """Peer-to-peer frontier exchange for k-sharded ranks (kbe_p2p_* in include/kbe200.h).
+
+    Every rank cudaMallocs one exchange buffer, the IPC handles are all-gathered over
+    torch.distributed, and each rank maps every peer's buffer.  The update kernel then
+    stores its new slice and control tail straight into all peers' buffers (NVLink) and
+    flags an epoch, replacing the per-iteration NCCL all-gather.  Used when every rank
+    can map every peer (KBE_P2P=0 forces the NCCL path); the decision is collective."""
+
+    def __init__(self, local, peers, rank):
+        self.local, self.peers, self.rank = local, peers, rank
+
+    @classmethod
+    def setup(cls, ws, rank: int, world: int):
+        import torch.distributed as dist
+        if os.environ.get("KBE_P2P", "1") == "0" or world > _lib.MAX_RANKS:
+            return None
+        L, p = _lib.lib(), ws.problem
+        nbytes = int(L.kbe_p2p_bytes(ws.problem_ptr(), world))
+        local, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        ok = L.kbe_p2p_alloc(nbytes, ctypes.byref(local), handle) == 0
+        handles = [None] * world
+        dist.all_gather_object(handles, handle.raw if ok else None)
+        peers = []
+        if all(h is not None for h in handles):
+            for r, h in enumerate(handles):
+                if r == rank:
+                    peers.append(local.value)
+                    continue
+                ptr = ctypes.c_void_p()
+                if L.kbe_p2p_open(h, ctypes.byref(ptr)) != 0:
+                    ok = False
+                    break
+                peers.append(ptr.value)
+        flags = [None] * world
+        dist.all_gather_object(flags, bool(ok and len(peers) == world))
+        ex = cls(local.value if local.value else None, peers, rank)
+        if not all(flags):       # every rank falls back to NCCL together
+            dist.barrier()
+            ex.close()
+            return None
+        p.p2p_world, p.p2p_rank, p.p2p_local = world, rank, local.value
+        for r, ptr in enumerate(peers):
+            p.p2p_peers[r] = ptr
+        return ex
+
+    def close(self, free_local: bool = True) -> None:
+        """Unmap the peers' buffers (after this rank's stream is idle).  The local buffer
+        is freed only when every rank is known to be done with it (free_local, after a
+        barrier); otherwise it is left allocated rather than risk a peer's late store."""
+        if self.local is None:
+            return
+        L = _lib.lib()
+        torch.cuda.synchronize()
+        for r, ptr in enumerate(self.peers):
+            if r != self.rank and ptr:
+                L.kbe_p2p_close(ptr)
+        if free_local:
+            L.kbe_p2p_free(self.local)
+        self.local, self.peers = None, []
+
+
 def _dist_info(schedule: Schedule):
     """(rank, world) of the k-shard group: torch.distributed when initialised."""
     import torch.distributed as dist
@@ -275,6 +337,9 @@ class PropagationDriver:
             hf=model.hf_mode == "on", interacting=self.interactions_on, dipole=complex(model.dipole),
             eps_v=eps_v, eps_c=eps_c, u_table=self.u_table, u_mid=u_mid, amp=amp,
             g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1)
+        self.p2p = None
+        if self.world > 1:
+            self.p2p = _PeerExchange.setup(self.ws, self.rank, self.world)
         _lib.check(_lib.lib().kbe_init_history(self.ws.problem_ptr(), stream_ptr()), "kbe_init_history")
         self.state = TwoTimeGF(nkl, self.k_lo, capacity, step_cfg.dt, g_hist, frontier=0)
         self.sigma = SigmaHistory(s_hist, capacity)
@@ -284,12 +349,21 @@ class PropagationDriver:
         # than the no-op launches they remove (profiles/r01/launch_modes.jsonl).
         self.use_graph = 1 if os.environ.get("KBE_GRAPH", "0") == "1" else 0
         if self.world > 1:
-            self._gather_frontier()
+            self.publish_initial()
 
     # ------------------------------------------------------------------ multi-rank plumbing
     def _gather_frontier(self) -> None:
-        """All-gather the new G slice (local k) into the all-k frontier buffer."""
-        all_gather_device(self.ws.front_all, self.ws.front_send)
+        """All-gather the new G slice (local k) into the all-k frontier buffer (NCCL path;
+        with the peer-to-peer exchange the update kernel has already stored it)."""
+        if self.p2p is None:
+            all_gather_device(self.ws.front_all, self.ws.front_send)
+
+    def publish_initial(self) -> None:
+        """Slice 0 (written by kbe_init_history) to every rank."""
+        if self.p2p is not None:
+            _lib.check(_lib.lib().kbe_p2p_publish(self.ws.problem_ptr(), stream_ptr()), "kbe_p2p_publish")
+        else:
+            all_gather_device(self.ws.front_all, self.ws.front_send)
 
     def _allreduce_hf(self) -> None:
         import torch.distributed as dist
@@ -406,7 +480,21 @@ class PropagationDriver:
     def synchronize(self) -> None:
         torch.cuda.current_stream().synchronize()
 
+    def close(self) -> None:
+        """Release the peer-exchange mappings once every rank is done with them
+        (collective when k-sharded)."""
+        if getattr(self, "p2p", None) is None:
+            return
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        if dist.is_initialized():
+            dist.barrier()
+        self.p2p.close()
+        self.p2p = None
+
     def __del__(self):
+        if getattr(self, "p2p", None) is not None:
+            self.p2p.close(free_local=False)   # no collective here: see close()
         ws = getattr(self, "ws", None)
         if ws is not None and getattr(self, "use_graph", 0):
             try:
@@ -420,4 +508,5 @@ def run(grid: KGrid, model: ModelConfig, step_cfg: StepConfig, schedule: Schedul
     """Propagate a fresh state for step_cfg.n_steps steps (propagator.py:395-406)."""
     driver = PropagationDriver(grid, model, step_cfg, schedule, pool)
     reports = driver.run(observer=observer)
+    driver.close()
     return driver.state, reports

@@ -58,5 +58,6 @@ def driver_worker(rank, world, port, outdir, n_k, n_steps):
     np.savez(os.path.join(outdir, f"drv{rank}.npz"), hist=drv.state.hist.cpu().numpy(),
              sig=drv.sigma.hist.cpu().numpy(), k_lo=drv.k_lo,
              its=np.array([r.iterations for r in reps]), dens=np.array([r.density for r in reps]),
-             drift=np.array([r.anticommutation_drift for r in reps]))
+             drift=np.array([r.anticommutation_drift for r in reps]), p2p=drv.p2p is not None)
+    drv.close()
     dist.destroy_process_group()
