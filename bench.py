@@ -341,8 +341,9 @@ def run_ours(args):
         for _ in range(args.steps):
             _reset(kb, drv)
             n1 = N
-            if world == 1:
-                _lib.check(_lib.lib().kbe_run(drv.ws.problem_ptr(), 1, n1, drv.use_graph, int(st.cuda_stream)))
+            if drv._device_sequenced():
+                _lib.check(_lib.lib().kbe_run(drv.ws.problem_ptr(), 1, n1, drv.use_graph if world == 1 else 0,
+                                              int(st.cuda_stream)))
             else:
                 for n in range(1, n1 + 1):
                     drv._launch_step(n)

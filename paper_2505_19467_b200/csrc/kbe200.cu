@@ -2382,8 +2382,10 @@ int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
 int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
-    if (sharded(*p) || p->front_send) {
-        snprintf(g_err, sizeof(g_err), "kbe_step drives one rank; multi-rank steps are sequenced by the host");
+    // one rank, or k-sharded ranks exchanging peer-to-peer (the update kernel publishes;
+    // nothing between launches).  NCCL-gathered or hf_mode="on" shards need the host.
+    if ((sharded(*p) && p->p2p_world <= 1) || (p->p2p_world > 1 && p->hf)) {
+        snprintf(g_err, sizeof(g_err), "kbe_step: these k-sharded steps need host collectives (NCCL path or hf_mode)");
         return KBE_ERR_ARG;
     }
     if (n < 1 || n > p->n_steps) { set_err("kbe_step: n", cudaSuccess); return KBE_ERR_ARG; }
@@ -2411,8 +2413,8 @@ int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_g
             if ((rc = kbe_step(p, n, stream))) return rc;
         return KBE_OK;
     }
-    if (sharded(*p) || p->front_send) {
-        snprintf(g_err, sizeof(g_err), "kbe_run drives one rank; multi-rank steps are sequenced by the host");
+    if (sharded(*p)) {
+        snprintf(g_err, sizeof(g_err), "kbe_run: the step graph drives one rank");
         return KBE_ERR_ARG;
     }
     if ((rc = ensure_attrs())) return rc;

@@ -370,10 +370,14 @@ class PropagationDriver:
         off = 208   # offsetof(kbe_ctl, hf_sum): 128 res + 64 nonfinite + 8 poisoned/pad, 16-aligned
         all_reduce_device(self.ws.ctl[off: off + 64].view(torch.float64), dist.ReduceOp.SUM)
 
+    def _device_sequenced(self) -> bool:
+        """One rank, or peer-to-peer shards without hf: the whole step is one C call."""
+        return self.world == 1 or (self.p2p is not None and self.model.hf_mode != "on")
+
     def _launch_step(self, n: int) -> None:
         L, P, st = _lib.lib(), self.ws.problem_ptr(), stream_ptr()
-        if self.world == 1:
-            _lib.check(L.kbe_run(P, n, n, self.use_graph, st), "kbe_run")
+        if self._device_sequenced():
+            _lib.check(L.kbe_run(P, n, n, self.use_graph if self.world == 1 else 0, st), "kbe_run")
             return
         # k-sharded step: same launch sequence, with one NCCL all-gather after every
         # update.  It carries the new G slice (the Sigma input needs all k) and each
@@ -456,8 +460,9 @@ class PropagationDriver:
             return []
         self._precheck(n0)
         n1 = min(last, self.capacity)
-        if self.world == 1:
-            _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, self.use_graph, stream_ptr()), "kbe_run")
+        if self._device_sequenced():
+            _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, self.use_graph if self.world == 1 else 0,
+                                          stream_ptr()), "kbe_run")
         else:
             for n in range(n0, n1 + 1):
                 self._launch_step(n)
