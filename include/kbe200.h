@@ -97,6 +97,17 @@ typedef struct kbe_problem {
     void* lc_part;        /* [k_local][nbb][N+1][4]: I< column, row-direction sums  */
     void* gc_part_c;      /* [k_local][nsb][N+1][4]: I> column, column-direction    */
     void* lc_part_c;      /* [k_local][nsb][N+1][4]: I< column, column-direction    */
+    /* incremental collision evaluations (as-printed; NULL g_sh disables them): a
+     * repeated evaluation at the same frontier whose vectors moved by <= 1e-7 since the
+     * last full one writes M_fp32 * (v - v_prev) into delta slots instead of
+     * re-streaming M in FP64. */
+    void* g_sh;           /* [k_local][tri] complex64 shadow of the final G slices   */
+    void* s_sh;           /* [k_local][tri] complex64 shadow of the final Sigma slices */
+    void* v_prev;         /* [k_local][2][8*plane_len(N)]: G and Sigma frontier of the last full evaluation */
+    void* fcol_part;      /* [k_local][N+1][4]: column-direction sums of the frontier slice */
+    void* row_delta;      /* incremental evaluations' M_fp32 dv, same shapes as row_part, */
+    void* col_delta;      /* col_part and gc_part; K3 adds them to the full evaluation's  */
+    void* gc_delta;       /* partials while the last evaluation was incremental          */
     /* peer-to-peer exchange over NVLink (p2p_world > 1; front_send / front_all are
      * then unused except for the initial slice): every rank owns a kbe_p2p_bytes()
      * buffer, opened by every peer through kbe_p2p_export / kbe_p2p_open. */

@@ -23,7 +23,13 @@
 
 #include "../../include/kbe200.h"
 
-#define KBE_ABI_VERSION 7
+// timing experiments only (profiles/coll_variants.sh; results are wrong): 1 = no 2x2
+// products, 2 = no warp reduction, 3 = no proxy fence before a ring refill, 4 = no row stores
+#ifndef KBE_COLL_EXP
+#define KBE_COLL_EXP 0
+#endif
+
+#define KBE_ABI_VERSION 8
 
 typedef double2 cplx;
 
@@ -37,7 +43,11 @@ struct kbe_ctl {
     unsigned task_next;                    // collision work queue head (reset by the last CTA)
     unsigned task_done;
     unsigned upd_done;                     // update CTAs finished (graph mode; reset by the last CTA)
-    unsigned pad2;
+    int prev_f1;                           // 1 + frontier of the last collision evaluation (0: none)
+    int full_f1;                           // 1 + frontier of the last full (FP64) evaluation
+    int incr_last;                         // the last evaluation was incremental (K3 adds the delta slots)
+    int pad3;
+    double dsum;                           // sum of the frontier changes since the last full evaluation
 };
 
 static char g_err[512] = "";
@@ -195,6 +205,12 @@ static_assert(sizeof(KbeTail) <= KBE_TAIL_CPLX * sizeof(cplx), "control tail");
 __host__ __device__ __forceinline__ int64_t front_chunk(const kbe_problem& P) {
     return (int64_t)(P.k_hi - P.k_lo) * 8 * plane_len(P.n_steps) + KBE_TAIL_CPLX;
 }
+// v_prev: the G (which = 0) and Sigma (1) frontier slices of local k as the last
+// collision evaluation used them (incremental evaluations, see collision_kernel)
+__device__ __forceinline__ int64_t vprev_off(const kbe_problem& P, int kl, int which) {
+    return ((int64_t)kl * 2 + which) * 8 * plane_len(P.n_steps);
+}
+
 // Peer-to-peer exchange (p2p_world > 1, kbe_p2p_* in include/kbe200.h): every rank owns
 // one buffer [2 parities][ranks][chunk] + flags[ranks] + epoch.  The update kernel
 // writes its new slice and control tail straight into every peer's buffer over
@@ -636,7 +652,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 // order this thread's prior generic-proxy shared accesses before later async-proxy (TMA) ones
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+#if KBE_COLL_EXP != 3
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+}
 // L2 policies: the history stream is read once per evaluation (evict first); the
 // K2 -> K3 partial sums must survive that stream in L2 (evict last).
 __device__ __forceinline__ uint64_t l2_evict_first() {
@@ -670,6 +690,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // most of the 148 SMs idle).  Column-direction partials are kept per ts-chunk in
 // KBE_COL_CHUNK-granular slots; the consumer (K3) derives the same ts from n.
 // langreth keeps ts = 32.
+// as-printed task height cap (slices per warp task; the per-slice vectors in shared
+// memory are sized by it) and the collision kernel's resident-CTA target
+#ifndef KBE_VEC_TS
+#define KBE_VEC_TS 16
+#endif
+#ifndef KBE_COLL_MINB
+#define KBE_COLL_MINB 16
+#endif
 #ifndef KBE_COLL_TASKS
 #define KBE_COLL_TASKS 16384
 #endif
@@ -680,22 +708,25 @@ __host__ __device__ __forceinline__ int coll_tiles(int n, int nkl) {
 __host__ __device__ __forceinline__ int coll_ts(int n, int nkl, int limit_mode) {
     if (limit_mode) return TS;
     const int tiles = coll_tiles(n, nkl);
-    if (tiles >= KBE_COLL_TASKS) return 32;
+    if (tiles >= KBE_COLL_TASKS) return KBE_VEC_TS;
     if (2 * tiles >= KBE_COLL_TASKS) return 16;
     return KBE_COL_CHUNK;
 }
 
 #ifndef KBE_STAGES
-#define KBE_STAGES 3
-#endif
-// timing experiments only (profiles/coll_variants.sh): 1 = no 2x2 products, 2 = no warp reduction
-#ifndef KBE_COLL_EXP
-#define KBE_COLL_EXP 0
+#define KBE_STAGES 2
 #endif
 // dynamic shared memory of one collision warp-task
 struct CollSmem {
-    cplx buf[KBE_STAGES][8][32];   // ring of slice cells: 8 planes x 32 points
-    cplx vec[TS][8];               // per-slice frontier vectors (Sigma part)
+    cplx buf[KBE_STAGES][8][32];   // ring of slice cells: 8 planes x 32 points (FP64), or
+                                   // 2 x KBE_STAGES complex64 shadow blocks (incremental)
+    cplx vec[KBE_VEC_TS][8];       // per-slice frontier vectors (Sigma part)
+    uint64_t bar[2 * KBE_STAGES];
+};
+// the langreth variant keeps 32-slice tasks
+struct CollSmemL {
+    cplx buf[KBE_STAGES][8][32];
+    cplx vec[TS][8];
     uint64_t bar[KBE_STAGES];
 };
 
@@ -757,15 +788,85 @@ __device__ __forceinline__ CollTask coll_task(int task, int nkl, int T0, int T1,
     return t;
 }
 
-// One warp = one task of 32 history points x 32 slices; a persistent grid of 1-warp
+// ---- incremental evaluations (as-printed) ------------------------------------------
+// Every evaluation at frontier f is I = H(v) + F(v): H the cells of slices < f (final
+// history, linear in the frontier vectors v = (G slice f, Sigma slice f)), F the cells
+// of slice f.  A full evaluation streams the FP64 history and snapshots v into v_prev.
+// A repeated evaluation at the same f (the predictor's I(n-1) after the previous
+// step's last corrector, or corrector it >= 1) whose vectors moved by at most
+// KBE_INCR_MAX_DELTA since that full one (the sum of the residuals the updates
+// measured in between) writes
+//   M (v - v_prev)   into delta slots, M streamed from a complex64 shadow of the history
+// (half the bytes; error |M| |dv| 2^-24 <= 6e-15 |I|, below a 50-ulp FP64 sum), and F(v)
+// exactly in FP64.  K3 then sums base + delta per slot.  Slice f's column-direction sums
+// live in their own slot (fcol_part), so the chunk slots hold H only.  The shadow of
+// slice n-1 (G and Sigma) is written by the predictor update, once it is final.
+#ifndef KBE_INCR_MAX_DELTA
+#define KBE_INCR_MAX_DELTA 1e-7
+#endif
+// frontier change since the previous evaluation at f: the residual its update measured
+__device__ __forceinline__ double coll_delta(const kbe_problem& P, const kbe_ctl* ctl, int it) {
+    if (it > 0) return __longlong_as_double((long long)res_bits(P, ctl, it - 1));
+    // predictor evaluation at the previous step's frontier: that step's final residual
+    double d = __longlong_as_double((long long)res_bits(P, ctl, P.max_iter - 1));
+    for (int i = 0; i < P.max_iter; ++i) {
+        const double r = __longlong_as_double((long long)res_bits(P, ctl, i));
+        if (r <= P.eps) { d = r; break; }
+    }
+    return d;
+}
+__device__ __forceinline__ bool coll_incremental(const kbe_problem& P, const kbe_ctl* ctl, int f, double delta) {
+    if (!P.g_sh || P.limit_mode) return false;
+    const volatile kbe_ctl* c = ctl;
+    if (c->prev_f1 != f + 1 || c->full_f1 != f + 1) return false;
+    return c->dsum + delta <= KBE_INCR_MAX_DELTA;   // false for NaN
+}
+// complex64 block of shadow slice s (8 planes x 32 points, 2 KB)
+__device__ __forceinline__ void issue_shadow(const float2* sh, int s, int wb0, cplx (*dst)[32], uint64_t* bar,
+                                             uint64_t pol) {
+    mbar_expect_tx(bar, 8u * 32u * 8u);
+    bulk_g2s(dst[0], sh + slice_off(s) + sl_idx(0, wb0), 8u * 32u * 8u, bar, pol);
+}
+// lane's 8 planes of one stage: FP64 block or complex64 shadow block
+__device__ __forceinline__ void stage_cell(const cplx (*buf)[32], bool shadow, int lane, cplx* lo, cplx* up) {
+    if (shadow) {
+        const float2* f = reinterpret_cast<const float2*>(buf);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float2 a = f[c * 32 + lane], b = f[(4 + c) * 32 + lane];
+            lo[c] = make_double2(a.x, a.y);
+            up[c] = make_double2(b.x, b.y);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { lo[c] = buf[c][lane]; up[c] = buf[4 + c][lane]; }
+    }
+}
+// part-0 vectors at point b of the G frontier slice f: w_b A(b), w_b B(b) with
+// A(b) = G>(t_f,t_b) = -U(f,b)^dag (b < f) | U(f,f), B(b) = G<(t_f,t_b) = L(f,b)
+__device__ __forceinline__ void front_ab(const cplx* slice, int b, int f, double w, cplx* A, cplx* B) {
+    cplx u[4], l[4];
+    load_cell(slice, b, l, u);
+    if (b < f) neg_dag(A, u);
+    else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) A[c] = u[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { A[c] = cscale(A[c], w); B[c] = cscale(l[c], w); }
+}
+
+// One warp = one task of 32 history points x ts slices; a persistent grid of 1-warp
 // CTAs walks the task list (tasks of both triangles, all local k).  No CTA-level
-// barriers; a 3-stage TMA bulk-copy ring per warp keeps ~8 KB per warp in flight.
+// barriers; a 3-stage bulk-copy ring per warp keeps ~8 KB per warp in flight.
 // A converged iteration costs one tiny grid of early exits.
-__global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n, int it) {
+__global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
     if (kbe_skip(P, ctl, it)) return;
+    const double delta = coll_delta(P, ctl, it);
+    const bool incr = coll_incremental(P, ctl, n, delta);
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
@@ -777,12 +878,30 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
     const int per_k = (tri0 + tri1) * nsub;
     const int total = per_k * (P.k_hi - P.k_lo);
     uint64_t* bars = sm.bar;
+    // The ring is latency-bound (a stage is refilled only once consumed), so its depth in
+    // slices, not bytes, sets the rate: an incremental evaluation's 2 KB shadow blocks
+    // get twice as many stages in the same shared memory.
+    const int STG = incr ? 2 * KBE_STAGES : KBE_STAGES;
+    auto stage = [&](unsigned st) -> cplx (*)[32] {
+        return reinterpret_cast<cplx (*)[32]>(reinterpret_cast<unsigned char*>(sm.buf) + st * (incr ? 2048u : 4096u));
+    };
     if (lane == 0) {
-        for (int i = 0; i < KBE_STAGES; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < STG; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
     }
     __syncwarp();
     const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (P.g_sh && !incr) {
+        // full evaluation: snapshot the frontier vectors (G and Sigma slice n, local k)
+        // for the incremental evaluations that may follow at this frontier
+        const int64_t per = 8 * plane_len(n), tot = (int64_t)(P.k_hi - P.k_lo) * 2 * per;
+        for (int64_t i = blockIdx.x * 32 + lane; i < tot; i += (int64_t)gridDim.x * 32) {
+            const int kl = (int)(i / (2 * per)), which = (int)((i / per) & 1);
+            const int64_t e = i % per;
+            const cplx* src = (const cplx*)(which ? P.s_hist : P.g_hist) + (int64_t)kl * P.tri + slice_off(n);
+            ((cplx*)P.v_prev)[vprev_off(P, kl, which) + e] = src[e];
+        }
+    }
     unsigned gcount = 0;   // slices consumed by this CTA so far (ring position / parity)
     for (;;) {
         // dynamic work queue: balances the half-full diagonal tasks
@@ -800,55 +919,100 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
         const int b = wb0 + lane;
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        // frontier slice n (vector) and the streamed triangle
+        // frontier slice n (vector), its value at the previous evaluation, the streamed triangle
         const cplx* fr = (part == 0 ? G : S) + slice_off(n);
+        const cplx* fp = incr ? (const cplx*)P.v_prev + vprev_off(P, kl, part) : nullptr;
         const cplx* hist = part == 0 ? S : G;
+        const float2* hsh = (const float2*)(part == 0 ? P.s_sh : P.g_sh) + (incr ? (int64_t)kl * P.tri : 0);
+        auto issue = [&](int s, unsigned st) {
+            if (incr) issue_shadow(hsh, s, wb0, stage(st), &bars[st], pol_stream);
+            else issue_slice(hist, s, wb0, stage(st), &bars[st], pol_stream);
+        };
+        // slices through the ring: all, except an incremental evaluation's slice n (FP64,
+        // read directly at the end of the task)
+        const int mr = (incr && part == 0 && s1 == n) ? m - 1 : m;
         __syncwarp();
         if (lane == 0)
-            for (int i = 0; i < KBE_STAGES && i < m; ++i) {
-                const unsigned st = (gcount + i) % KBE_STAGES;
-                issue_slice(hist, s0 + i, wb0, sm.buf[st], &bars[st], pol_stream);
-            }
+            for (int i = 0; i < STG && i < mr; ++i) issue(s0 + i, (gcount + i) % STG);
         double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
+        double* outD = (double*)(part == 0 ? P.row_delta : P.gc_delta);
+        // row slot (bc, s): full evaluation -> base slot; incremental -> delta slot, except
+        // for slice n, which is always full (base slot, zero delta)
+        auto put_row = [&](int s, double rr) {
+            if (KBE_COLL_EXP != 4 && (lane & 3) == 0) {
+                const int64_t o = (((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2);
+                if (incr && s < n) {
+                    st_keep(&outD[o], rr, pol_keep);
+                } else {
+                    st_keep(&outP[o], rr, pol_keep);
+                    if (incr) st_keep(&outD[o], 0.0, pol_keep);
+                }
+            }
+        };
 
         if (part == 0) {
-            // per-slice vectors w_s A(s), w_s B(s);  A(s) = G>(t_n,t_s), B(s) = G<(t_n,t_s)
+            // per-slice vectors w_s A(s), w_s B(s) (incremental: their change since the last
+            // evaluation, except for slice n itself)
             if (lane < m) {
                 const int s = s0 + lane;
                 const double w = quad_w(n, s, dt, P.quad);
-                cplx u[4], l[4], a[4];
-                load_cell(fr, s, l, u);
-                if (s < n) neg_dag(a, u);
-                else {
+                cplx a[4], l[4];
+                front_ab(fr, s, n, w, a, l);
+                if (incr && s < n) {
+                    cplx a0[4], l0[4];
+                    front_ab(fp, s, n, w, a0, l0);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) a[c] = u[c];
+                    for (int c = 0; c < 4; ++c) { a[c] = csub(a[c], a0[c]); l[c] = csub(l[c], l0[c]); }
                 }
 #pragma unroll
-                for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = cscale(a[c], w); sm.vec[lane][4 + c] = cscale(l[c], w); }
+                for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = a[c]; sm.vec[lane][4 + c] = l[c]; }
             }
             cplx Ab[4], Bb[4], col[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { Ab[c] = cz(); Bb[c] = cz(); col[c] = cz(); }
+            const double wb = quad_w(n, b, dt, P.quad);
             if (b <= s1) {
-                const double w = quad_w(n, b, dt, P.quad);
-                cplx u[4], l[4];
-                load_cell(fr, b, l, u);
-                if (b < n) neg_dag(Ab, u);
-                else {
+                front_ab(fr, b, n, wb, Ab, Bb);
+                if (incr) {
+                    cplx a0[4], l0[4];
+                    front_ab(fp, b, n, wb, a0, l0);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) Ab[c] = u[c];
+                    for (int c = 0; c < 4; ++c) { Ab[c] = csub(Ab[c], a0[c]); Bb[c] = csub(Bb[c], l0[c]); }
                 }
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { Ab[c] = cscale(Ab[c], w); Bb[c] = cscale(l[c], w); }
             }
+            // column chunk slot (history part): base (full) or delta (incremental)
+            cplx* colP = (cplx*)(incr ? P.col_delta : P.col_part) + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
             __syncwarp();
-            for (int i = 0; i < m; ++i, ++gcount) {
+            for (int i = 0; i < m; ++i) {
                 const int s = s0 + i;
-                const unsigned st = gcount % KBE_STAGES;
-                mbar_wait(&bars[st], (gcount / KBE_STAGES) & 1u);
-                cplx SL[4], SU[4];
+                const bool ring = i < mr;
+                const unsigned st = gcount % STG;
+                if (s == n) {
+                    // frontier slice: its column sums go to their own slot; an incremental
+                    // evaluation switches to the full vectors for it
+                    if (b <= s1) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) { SL[c] = sm.buf[st][c][lane]; SU[c] = sm.buf[st][4 + c][lane]; }
+                        for (int c = 0; c < 4; ++c) st_keep2(&colP[c], cneg(col[c]), pol_keep);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) col[c] = cz();
+                    if (incr && b <= s1) front_ab(fr, b, n, wb, Ab, Bb);
+                }
+                cplx SL[4], SU[4];
+                if (ring) {
+                    mbar_wait(&bars[st], (gcount / STG) & 1u);
+                    stage_cell(stage(st), incr, lane, SL, SU);
+                    // the stage is in registers: refill it now, so the copy overlaps this
+                    // slice's arithmetic (proxy fence: generic reads before async writes)
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0 && i + STG < mr) issue(s + STG, st);
+                    ++gcount;
+                } else {   // incremental evaluation: slice n in FP64, straight from global
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) { SL[c] = cz(); SU[c] = cz(); }
+                    if (b <= s) load_cell(hist + slice_off(s), b, SL, SU);
+                }
                 cplx row[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) row[c] = cz();
@@ -884,30 +1048,42 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #else
                 const double rr = warp_rs8(v, lane);   // all lanes' reads of stage st are consumed here
 #endif
-                if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
-                // refill stage st only after every lane has consumed it (WAR across proxies)
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, s + KBE_STAGES, wb0, sm.buf[st], &bars[st], pol_stream);
+                put_row(s, rr);
             }
             if (b <= s1) {
-                cplx* colP = (cplx*)P.col_part;
+                if (s1 == n) {   // slice n's column sums (full in both modes)
+                    cplx* fc = (cplx*)P.fcol_part + ((int64_t)kl * N1 + b) * 4;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) st_keep2(&colP[(((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4 + c], cneg(col[c]), pol_keep);
+                    for (int c = 0; c < 4; ++c) st_keep2(&fc[c], cneg(col[c]), pol_keep);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) st_keep2(&colP[c], cneg(col[c]), pol_keep);
+                }
             }
         } else {
-            // column collision over the G triangle; frontier vectors X = SL(n,b), Y = SU(n,b)
+            // column collision over the G triangle (slices < n: all history); frontier
+            // vectors X = SL(n,b), Y = SU(n,b) (incremental: their change)
             cplx X[4], Y[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
-            if (b <= s1) load_cell(fr, b, X, Y);
+            if (b <= s1) {
+                load_cell(fr, b, X, Y);
+                if (incr) {
+                    cplx X0[4], Y0[4];
+                    load_cell(fp, b, X0, Y0);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) { X[c] = csub(X[c], X0[c]); Y[c] = csub(Y[c], Y0[c]); }
+                }
+            }
             for (int i = 0; i < m; ++i, ++gcount) {
                 const int j = s0 + i;
-                const unsigned st = gcount % KBE_STAGES;
-                mbar_wait(&bars[st], (gcount / KBE_STAGES) & 1u);
+                const unsigned st = gcount % STG;
+                mbar_wait(&bars[st], (gcount / STG) & 1u);
                 cplx GL[4], GU[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) { GL[c] = sm.buf[st][c][lane]; GU[c] = sm.buf[st][4 + c][lane]; }
+                stage_cell(stage(st), incr, lane, GL, GU);
+                fence_proxy_async();   // stage in registers: refill it during the arithmetic
+                __syncwarp();
+                if (lane == 0 && i + STG < m) issue(j + STG, st);
                 cplx acc[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[c] = cz();
@@ -942,20 +1118,26 @@ __global__ void __launch_bounds__(32, 16) collision_kernel(kbe_problem P, int n,
 #else
                 const double rr = warp_rs8(v, lane);
 #endif
-                if ((lane & 3) == 0) st_keep(&outP[(((int64_t)kl * P.nbb + bc) * N1 + j) * 8 + (lane >> 2)], rr, pol_keep);
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0 && i + KBE_STAGES < m) issue_slice(hist, j + KBE_STAGES, wb0, sm.buf[st], &bars[st], pol_stream);
+                put_row(j, rr);
             }
         }
     }
-    // last CTA out resets the queue for the next launch on this stream
+    // last CTA out resets the queue for the next launch on this stream and records the
+    // frontier whose partials are now in the workspace
     if (lane == 0) {
         __threadfence();
         const unsigned d = atomicAdd(&ctl->task_done, 1u);
         if (d == gridDim.x - 1) {
             ctl->task_next = 0u;
             ctl->task_done = 0u;
+            ctl->prev_f1 = n + 1;
+            if (incr) {
+                ctl->dsum += delta;
+            } else {
+                ctl->full_f1 = n + 1;
+                ctl->dsum = 0.0;
+            }
+            ctl->incr_last = incr ? 1 : 0;
             __threadfence();
         }
     }
@@ -982,7 +1164,7 @@ __global__ void __launch_bounds__(32, 8) collision_langreth_kernel(kbe_problem P
     if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
     if (kbe_skip(P, ctl, it)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
-    CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
+    CollSmemL& sm = *reinterpret_cast<CollSmemL*>(smraw);
     const int lane = threadIdx.x;
     const int N1 = P.n_steps + 1;
     const double dt = P.dt;
@@ -1204,17 +1386,33 @@ __device__ __forceinline__ void reduce_chunks(const kbe_problem& P, const void* 
         for (int sc = l / ts; sc <= s_hi; ++sc)
 #pragma unroll
             for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], cp[sc * N1 * 4 + c]);
+        if (coldir == P.col_part && !P.limit_mode && l < nf) {   // frontier slice (own slot)
+            const cplx* fc = (const cplx*)P.fcol_part + ((int64_t)kl * N1 + l) * 4;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], fc[c]);
+        }
     }
 }
 // I<(t_nf, t_l) / I>(t_nf, t_l) (rows) and I>(t_j, t_nf) / I<(t_j, t_nf) (columns)
+// + the delta slots when the last evaluation was incremental (as-printed only)
+__device__ __forceinline__ void add_deltas(const kbe_problem& P, const void* rowd, const void* cold, int kl, int l,
+                                           int nf, cplx* out) {
+    if (P.limit_mode || !P.ctl || !((const volatile kbe_ctl*)P.ctl)->incr_last) return;
+    cplx d[4];
+    reduce_chunks(P, rowd, cold, kl, l, nf, d);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], d[c]);
+}
 __device__ __forceinline__ void reduce_lr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
     reduce_chunks(P, P.row_part, P.col_part, kl, l, nf, out);
+    add_deltas(P, P.row_delta, P.col_delta, kl, l, nf, out);
 }
 __device__ __forceinline__ void reduce_gr(const kbe_problem& P, int kl, int l, int nf, cplx* out) {
     reduce_chunks(P, P.row_part_g, P.col_part_g, kl, l, nf, out);
 }
 __device__ __forceinline__ void reduce_gc(const kbe_problem& P, int kl, int j, int nf, cplx* out) {
     reduce_chunks(P, P.gc_part, P.limit_mode ? P.gc_part_c : nullptr, kl, j, nf, out);
+    add_deltas(P, P.gc_delta, nullptr, kl, j, nf, out);
 }
 __device__ __forceinline__ void reduce_lc(const kbe_problem& P, int kl, int j, int nf, cplx* out) {
     reduce_chunks(P, P.lc_part, P.lc_part_c, kl, j, nf, out);
@@ -1370,6 +1568,9 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
 // does not carry the langreth reductions' registers.
 // Points per CTA: up to 4 (and <= 512 threads), but small frontiers keep one point
 // per CTA so that the grid still spreads over the SMs.
+#ifndef KBE_UPD_BATCH
+#define KBE_UPD_BATCH 4   // partial loads in flight per operand and thread in K3
+#endif
 static int g_upd_min_ctas = -1;   // KBE_UPD_MIN_CTAS (tuning knob)
 static int upd_ppc(int nkl, int n) {
     if (g_upd_min_ctas < 0) {
@@ -1493,8 +1694,13 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         const int na = nr + ns, ng = b < nf ? (LANG ? nr + ns : nr) : 0;
         // UPD_BATCH independent loads per operand in flight before the in-order adds
         // (the sum order, and so the result, does not depend on the batch size)
-        constexpr int UPD_BATCH = 4;
+        constexpr int UPD_BATCH = KBE_UPD_BATCH;
         cplx a = cz(), g = cz();
+        // after an incremental evaluation every slot is base + delta (collision_kernel)
+        const bool dl = !LANG && ((const volatile kbe_ctl*)ctl)->incr_last;
+        const cplx* rowD = dl ? (const cplx*)P.row_delta + rb : nullptr;
+        const cplx* colD = dl ? (const cplx*)P.col_delta + cb : nullptr;
+        const cplx* gcD = dl ? (const cplx*)P.gc_delta + rb : nullptr;
         for (int i0 = 0; i0 < na || i0 < ng; i0 += UPD_BATCH) {
             cplx va[UPD_BATCH], vg[UPD_BATCH];
 #pragma unroll
@@ -1502,6 +1708,10 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 const int q = i0 + u;
                 va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
                 vg[u] = q < ng ? (q < nr ? gcP[q * cs] : gcC[(c0 + q - nr) * cs]) : cz();
+                if (dl) {
+                    if (q < na) va[u] = cadd(va[u], q < nr ? rowD[q * cs] : colD[(c0 + q - nr) * cs]);
+                    if (q < ng) vg[u] = cadd(vg[u], gcD[q * cs]);
+                }
             }
 #pragma unroll
             for (int u = 0; u < UPD_BATCH; ++u) {
@@ -1509,6 +1719,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 if (i0 + u < ng) g = cadd(g, vg[u]);
             }
         }
+        if (!LANG && b < nf)   // the frontier slice's column-direction sums (own slot)
+            a = cadd(a, ((const cplx*)P.fcol_part)[((int64_t)kl * N1 + b) * 4 + c]);
         sA[(o * nkl + kl) * 4 + c] = a;
         sB[(o * nkl + kl) * 4 + c] = g;
     }
@@ -1592,6 +1804,18 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             fin = fin && isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
         }
         if (b == n - 1) { sRow[kl * 4 + c] = row; sCol[kl * 4 + c] = col; }
+        if (P.g_sh && phase == 0) {      // slice n-1 is final (G and Sigma): complex64 shadow
+            const int64_t so = (int64_t)kl * P.tri + slice_off(n - 1);
+            const cplx* sp = (const cplx*)P.s_hist + so;
+            float2* gsh = (float2*)P.g_sh + so;
+            float2* ssh = (float2*)P.s_sh + so;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t e = sl_idx(4 * h + c, b);
+                gsh[e] = make_float2((float)prev[e].x, (float)prev[e].y);
+                ssh[e] = make_float2((float)sp[e].x, (float)sp[e].y);
+            }
+        }
         cur[sl_idx(c, b)] = row;
         cur[sl_idx(4 + c, b)] = col;
         publish_entry(P, kl, c, b, row, pm, e_next);
@@ -1979,10 +2203,10 @@ static int ensure_attrs() {
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
-    e = cudaFuncSetAttribute(collision_langreth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
+    e = cudaFuncSetAttribute(collision_langreth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmemL));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision_langreth)", e); return KBE_ERR_CUDA; }
     int occ = 0, occ2 = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, collision_langreth_kernel, 32, sizeof(CollSmem));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, collision_langreth_kernel, 32, sizeof(CollSmemL));
     if (e != cudaSuccess || occ2 < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(langreth)", e); return KBE_ERR_CUDA; }
     g_lang_occ = occ2;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, collision_kernel, 32, sizeof(CollSmem));
@@ -2016,6 +2240,11 @@ static int check_problem(const kbe_problem* p) {
         return KBE_ERR_UNSUPPORTED;
     }
     if (!p->phi) { set_err("kbe_problem.phi", cudaSuccess); return KBE_ERR_ARG; }
+    if ((!p->limit_mode && !p->fcol_part) ||
+        (p->g_sh && (!p->s_sh || !p->v_prev || !p->row_delta || !p->col_delta || !p->gc_delta))) {
+        snprintf(g_err, sizeof(g_err), "kbe_problem: fcol_part / incremental-evaluation buffers missing");
+        return KBE_ERR_ARG;
+    }
     if (p->p2p_world > 1 && (p->p2p_world > KBE_MAX_RANKS || !p->p2p_local || p->p2p_rank < 0 ||
                              p->p2p_rank >= p->p2p_world || p->n_k % p->p2p_world ||
                              (p->k_hi - p->k_lo) * p->p2p_world != p->n_k)) {
@@ -2040,7 +2269,7 @@ static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
         const int T0 = n / TS + 1;
         const int64_t tl = 2 * (int64_t)(T0 * (T0 + 1) / 2) * nkl;
         const int64_t cl = (int64_t)g_num_sms * g_lang_occ;
-        make_spec(s, collision_langreth_kernel, dim3((int)(tl < cl ? tl : cl)), dim3(32), sizeof(CollSmem), *p, n, it);
+        make_spec(s, collision_langreth_kernel, dim3((int)(tl < cl ? tl : cl)), dim3(32), sizeof(CollSmemL), *p, n, it);
         return;
     }
     const int64_t total = (int64_t)coll_tiles(n, nkl) * (TS / coll_ts(n, nkl, 0));

@@ -150,7 +150,7 @@ class _Workspace:
 
     def __init__(self, *, n_k, k_lo, k_hi, n_steps, dt, eps, max_iter, quad, limit_mode, hf,
                  interacting, dipole, eps_v, eps_c, u_table, u_mid, amp, g_hist, s_hist, device,
-                 multi_rank=False):
+                 multi_rank=False, incremental=False):
         N1 = n_steps + 1
         kl = k_hi - k_lo
         self.nbb = -(-N1 // _lib.TILE_B)
@@ -165,6 +165,15 @@ class _Workspace:
         self.ctl = torch.zeros(int(_lib.lib().kbe_ctl_bytes()), dtype=torch.uint8, device=device)
         self.reports = torch.zeros((N1, _lib.REPORT_W), dtype=torch.float64, device=device)
         self.phi = torch.zeros((N1, kl, 4), **c128)
+        self.fcol_part = torch.zeros((kl, N1, 4), **c128)
+        # incremental collision evaluations (as-printed): complex64 shadows of the final
+        # history slices and the frontier the last evaluation used (include/kbe200.h)
+        self.g_sh = self.s_sh = self.v_prev = None
+        if incremental and not limit_mode:
+            self.g_sh = torch.zeros_like(g_hist, dtype=torch.complex64)
+            self.s_sh = torch.zeros_like(s_hist, dtype=torch.complex64)
+            self.v_prev = torch.zeros((kl, 2, 8 * _lib.plane_len(n_steps)), **c128)
+            self.deltas = [torch.zeros_like(t) for t in (self.row_part, self.col_part, self.gc_part)]
         self.lang = None
         if limit_mode:   # langreth: I> rows and I< columns kept separately, both directions
             shapes = (self.nbb, self.nsb, self.nbb, self.nsb, self.nsb)   # row_g, col_g, lc, gc_c, lc_c
@@ -200,6 +209,10 @@ class _Workspace:
         p.phi = self.phi.data_ptr()
         if self.lang is not None:
             (p.row_part_g, p.col_part_g, p.lc_part, p.gc_part_c, p.lc_part_c) = [t.data_ptr() for t in self.lang]
+        p.fcol_part = self.fcol_part.data_ptr()
+        if self.g_sh is not None:
+            p.g_sh, p.s_sh, p.v_prev = self.g_sh.data_ptr(), self.s_sh.data_ptr(), self.v_prev.data_ptr()
+            p.row_delta, p.col_delta, p.gc_delta = [t.data_ptr() for t in self.deltas]
         self.problem = p
 
     def problem_ptr(self) -> int:
@@ -287,6 +300,17 @@ class _PeerExchange:
         self.local, self.peers = None, []
 
 
+def _incremental_default(n_k: int) -> bool:
+    """Incremental collision evaluations (collision_kernel): KBE_INCR=1/0 forces them on /
+    off; by default on for n_k >= 32, where K2 has enough tasks per launch to be closer
+    to HBM-bound and half-byte evaluations pay (profiles/r01/incr_ab_v17.jsonl: cfg3
+    +3.6 %, cfg2 -0.7 %)."""
+    env = os.environ.get("KBE_INCR")
+    if env in ("0", "1"):
+        return env == "1"
+    return n_k >= 32
+
+
 def _dist_info(schedule: Schedule):
     """(rank, world) of the k-shard group: torch.distributed when initialised."""
     import torch.distributed as dist
@@ -336,7 +360,8 @@ class PropagationDriver:
             eps=step_cfg.eps, max_iter=step_cfg.max_iter, quad=quad, limit_mode=limit,
             hf=model.hf_mode == "on", interacting=self.interactions_on, dipole=complex(model.dipole),
             eps_v=eps_v, eps_c=eps_c, u_table=self.u_table, u_mid=u_mid, amp=amp,
-            g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1)
+            g_hist=g_hist, s_hist=s_hist, device=dev, multi_rank=self.world > 1,
+            incremental=_incremental_default(grid.n_k))
         self.p2p = None
         if self.world > 1:
             self.p2p = _PeerExchange.setup(self.ws, self.rank, self.world)

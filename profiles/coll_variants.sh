@@ -1,15 +1,12 @@
 #!/bin/bash
-# Build timing-only variants of the collision kernel into scratch/ (never shipped):
-#   exp1 = streaming + reductions without the 2x2 products, exp2 = products without
-#   the warp reduction, st2/st4 = 2/4-stage TMA ring.  Run profiles/kernel_ab.py with
-#   KBE_LIB=scratch/<variant>.so to compare against the product library.
+# Build timing-only variants of the collision kernel into scratch/ (never shipped; their
+# results are wrong): exp1 = no 2x2 products, exp2 = no warp reduction, exp3 = no proxy
+# fence before a ring refill, exp4 = no row-partial stores.  Run profiles/kernel_ab.py or
+# profiles/incr_ab.py with KBE_LIB=scratch/<variant>.so to compare with the product.
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p scratch
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -I include"
 SRC=paper_2505_19467_b200/csrc/kbe200.cu
-nvcc $F -DKBE_COLL_EXP=1 -o scratch/exp1.so $SRC &
-nvcc $F -DKBE_COLL_EXP=2 -o scratch/exp2.so $SRC &
-nvcc $F -DKBE_STAGES=2 -o scratch/st2.so $SRC &
-nvcc $F -DKBE_STAGES=4 -o scratch/st4.so $SRC &
+for v in ${VARIANTS:-1 2 3 4}; do nvcc $F -DKBE_COLL_EXP=$v -o scratch/exp$v.so $SRC & done
 wait

@@ -1,0 +1,77 @@
+"""Isolated K2 timing, full vs incremental evaluation, at one frontier.
+
+    python profiles/incr_ab.py [--workload cfg2] [--n 900] [--reps 20]
+
+Propagates to step n-1, runs step n's predictor and first corrector, then times
+repeated corrector-1 collision launches at frontier n with the iteration-0 residual
+forced to 1e-3 (full FP64 evaluation) and to 2e-9 (incremental: complex64 history
+shadow + FP64 frontier slice).  Timing only: the forced residual is not physical.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import struct
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="cfg2", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--n", type=int, default=900)
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    cfgw = bench.select_workload(args.workload)
+    import paper_2505_19467_b200 as kb
+    from paper_2505_19467_b200 import _lib
+    from paper_2505_19467_b200._device import stream_ptr
+
+    torch.cuda.set_device(0)
+    model = kb.ModelConfig(**bench.model_kwargs(cfgw))
+    cfg = kb.StepConfig(dt=cfgw["dt"], n_steps=cfgw["n_steps"], memory_budget=1 << 40)
+    drv = kb.PropagationDriver(kb.build_kgrid(cfgw["n_k"]), model, cfg)
+    L, P, sp = _lib.lib(), drv.ws.problem_ptr(), stream_ptr()
+    st = torch.cuda.current_stream()
+    n = args.n
+    _lib.check(L.kbe_run(P, 1, n - 1, 0, sp))
+    for f, it, ph in ((n - 1, 0, 0), (n, 0, 1)):
+        _lib.check(L.kbe_sigma_frontier(P, f, it, sp))
+        _lib.check(L.kbe_collision_frontier(P, f, it, sp))
+        _lib.check(L.kbe_update(P, n, ph, 0, sp))
+    torch.cuda.synchronize()
+    res = drv.ws.ctl[0: 8 * _lib.MAX_ITER].view(torch.int64)
+
+    def timed(r0):
+        res[0] = struct.unpack("<q", struct.pack("<d", r0))[0]
+        for _ in range(3):
+            _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.reps):
+            _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        e1.record(st)
+        torch.cuda.synchronize()
+        return 1e3 * e0.elapsed_time(e1) / args.reps
+
+    nk = cfgw["n_k"]
+    full_b = 64.0 * nk * ((n + 1) * (n + 2) + n * (n + 1))
+    incr_b = 32.0 * nk * (n * (n + 1) + n * (n + 1)) + 64.0 * nk * (n + 1)   # shadow + FP64 slice n
+    out = {"workload": args.workload, "n": n, "lib": os.environ.get("KBE_LIB", "product")}
+    out["full_us"] = timed(1e-3)
+    out["incr_us"] = timed(2e-9)   # > eps (not converged); 23 launches accumulate 4.6e-8 <= KBE_INCR_MAX_DELTA
+    out["full_gbs"] = full_b / (out["full_us"] * 1e-6) / 1e9
+    out["incr_gbs"] = incr_b / (out["incr_us"] * 1e-6) / 1e9
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -279,3 +279,23 @@ def test_graph_path_equals_stream_path(name, monkeypatch):
     rc = [c.step() for _ in range(int(g["n_steps"]))]
     assert [r.iterations for r in rc] == [r.iterations for r in rb]
     assert torch.equal(c.state.hist, b.state.hist)
+
+
+@pytest.mark.parametrize("name", ["traj_nk16.npz", "traj_simpson.npz", "traj_nk64_synth.npz"])
+def test_incremental_evaluations_match_full_evaluations(name, monkeypatch):
+    """Repeated collision evaluations at one frontier with |dv| <= 1e-7 add M_fp32 dv to
+    the previous partials (collision_kernel, incremental mode); the trajectory equals the
+    all-FP64 one to 1e-13 with the same iteration counts."""
+    g = load_golden(name)
+    monkeypatch.setenv("KBE_INCR", "0")
+    a = _driver_from_fixture(g)
+    assert a.ws.g_sh is None
+    ra = a.run()
+    monkeypatch.setenv("KBE_INCR", "1")
+    b = _driver_from_fixture(g)
+    assert b.ws.g_sh is not None
+    rb = b.run()
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    scale = float(a.state.hist.abs().max())
+    assert float((a.state.hist - b.state.hist).abs().max()) <= 1e-13 * scale
+    assert float((a.sigma.hist - b.sigma.hist).abs().max()) <= 1e-13 * float(a.sigma.hist.abs().max())
