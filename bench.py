@@ -291,14 +291,36 @@ def _collision_roofline(kb, drv, hbm_peak):
     torch.cuda.synchronize()
     rows = drv.ws.reports.cpu().numpy()
     iters = rows[1:, 1].astype(int)
-    tot_b, tot_t, launches = 0.0, 0.0, 0
+    hist = rows[1:, 8: 8 + _lib.MAX_ITER]
+    eps = drv.cfg.eps
+
+    def final_res(step):                      # residual of the step's last corrector
+        h = hist[step - 1][: iters[step - 1]]
+        return float(h[-1])
+
+    # mirror of the device's incremental-evaluation rule (collision_kernel)
+    incr_on = drv.ws.g_sh is not None
+    prev_f = full_f = -1
+    dsum = 0.0
+    tot_b, tot_t, launches, n_incr = 0.0, 0.0, 0, 0
     for n, ci, nf, e0, e1 in ev:
         if ci > iters[n - 1]:
             continue    # converged: launch was a no-op
-        # algorithmic bytes: each unique 2x2 c128 block of the Sigma triangle (slices 0..nf,
-        # both functions) and of the G triangle (slices 0..nf-1, both functions) read once
-        blocks = 2 * (nf + 1) * (nf + 2) // 2 + 2 * nf * (nf + 1) // 2
-        tot_b += 64.0 * nk * blocks
+        it = 0 if ci == 0 else ci - 1
+        delta = (final_res(nf) if nf >= 1 else float("inf")) if ci == 0 else (float(hist[n - 1][it - 1]) if it else float("inf"))
+        incr = incr_on and prev_f == nf and full_f == nf and dsum + delta <= 1e-7
+        prev_f = nf
+        if incr:
+            dsum += delta
+            n_incr += 1
+            # complex64 shadow of both triangles' slices < nf (64 B per cell) + FP64 slice nf
+            tot_b += nk * (64.0 * nf * (nf + 1) + 128.0 * (nf + 1))
+        else:
+            full_f, dsum = nf, 0.0
+            # algorithmic bytes: each unique 2x2 c128 block of the Sigma triangle (slices
+            # 0..nf, both functions) and of the G triangle (slices 0..nf-1) read once
+            blocks = 2 * (nf + 1) * (nf + 2) // 2 + 2 * nf * (nf + 1) // 2
+            tot_b += 64.0 * nk * blocks
         tot_t += e0.elapsed_time(e1) * 1e-3
         launches += 1
     step_s = t_total0.elapsed_time(t_total1) * 1e-3
@@ -306,6 +328,7 @@ def _collision_roofline(kb, drv, hbm_peak):
     return {
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
         "traffic": None, "kernel": "collision_kernel (K2)", "launches_with_work": launches,
+        "incremental_launches": n_incr,
         "kernel_seconds": tot_t, "share_of_propagation": tot_t / step_s,
         "bytes_per_launch_formula": "64*n_k*[(n+1)(n+2) + n(n+1)]",
     }, iters

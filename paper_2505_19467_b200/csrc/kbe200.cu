@@ -246,37 +246,51 @@ __device__ __forceinline__ cplx* p2p_dst(const kbe_problem& P, int r, unsigned l
     return (cplx*)P.p2p_peers[r] + ((int64_t)(e & 1) * P.p2p_world + P.p2p_rank) * front_chunk(P);
 }
 // consumer side: block until every rank has published the local epoch
+__device__ __noinline__ void p2p_wait_ranks(const unsigned long long* flags, int world) {
+    if (threadIdx.x == 0) {
+        const unsigned long long e = *(volatile const unsigned long long*)(flags + world);
+        for (int r = 0; r < world; ++r)
+            while (ld_acquire_sys(flags + r) < e) __nanosleep(64);
+    }
+}
 __device__ __forceinline__ void p2p_wait(const kbe_problem& P) {
     if (P.p2p_world <= 1) return;
-    if (threadIdx.x == 0) {
-        const unsigned long long e = p2p_epoch(P);
-        const unsigned long long* f = p2p_flags(P, P.p2p_local);
-        for (int r = 0; r < P.p2p_world; ++r)
-            while (ld_acquire_sys(f + r) < e) __nanosleep(64);
-    }
+    p2p_wait_ranks(p2p_flags(P, P.p2p_local), P.p2p_world);
     __syncthreads();
 }
 // producer side (one thread, after every CTA's stores were fenced): epoch + 1 everywhere
+// (rank loops are unrolled to KBE_MAX_RANKS so that p2p_peers[] is indexed by
+// constants; a runtime index into a kernel parameter forces a local copy of it)
 __device__ __forceinline__ void p2p_signal(const kbe_problem& P, unsigned long long e) {
     __threadfence_system();
     *(volatile unsigned long long*)(p2p_flags(P, P.p2p_local) + P.p2p_world) = e;
-    for (int r = 0; r < P.p2p_world; ++r) st_release_sys(p2p_flags(P, P.p2p_peers[r]) + P.p2p_rank, e);
+#pragma unroll
+    for (int r = 0; r < KBE_MAX_RANKS; ++r)
+        if (r < P.p2p_world) st_release_sys(p2p_flags(P, P.p2p_peers[r]) + P.p2p_rank, e);
 }
 __device__ __forceinline__ const KbeTail* rank_tail(const kbe_problem& P, int r) {
     return (const KbeTail*)(front_base(P) + r * front_chunk(P) + front_chunk(P) - KBE_TAIL_CPLX);
 }
-// residual bits / non-finite flag of iteration i over all ranks
-__device__ __forceinline__ unsigned long long res_bits(const kbe_problem& P, const kbe_ctl* ctl, int i) {
-    if (!sharded(P)) return ctl->res[i];
+// residual bits / non-finite flag of iteration i over all ranks.  The multi-rank paths
+// are out of line: inlined, their loops cost the hot kernels registers.
+// (scalar arguments only: a kernel-parameter struct passed by reference would be copied
+// to local memory)
+__device__ __noinline__ unsigned long long res_bits_ranks(const cplx* base, int64_t chunk, int R, int i) {
     unsigned long long m = 0;
-    for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) m = max(m, rank_tail(P, r)->res[i]);
+    for (int r = 0; r < R; ++r) m = max(m, ((const KbeTail*)(base + r * chunk + chunk - KBE_TAIL_CPLX))->res[i]);
     return m;
 }
-__device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl* ctl, int i) {
-    if (!sharded(P)) return ctl->nonfinite[i];
+__device__ __noinline__ int nonfinite_ranks(const cplx* base, int64_t chunk, int R, int i) {
     int f = 0;
-    for (int r = 0, R = P.n_k / (P.k_hi - P.k_lo); r < R; ++r) f |= rank_tail(P, r)->nonfinite[i];
+    for (int r = 0; r < R; ++r) f |= ((const KbeTail*)(base + r * chunk + chunk - KBE_TAIL_CPLX))->nonfinite[i];
     return f;
+}
+__device__ __forceinline__ unsigned long long res_bits(const kbe_problem& P, const kbe_ctl* ctl, int i) {
+    return sharded(P) ? res_bits_ranks(front_base(P), front_chunk(P), P.n_k / (P.k_hi - P.k_lo), i) : ctl->res[i];
+}
+__device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl* ctl, int i) {
+    return sharded(P) ? nonfinite_ranks(front_base(P), front_chunk(P), P.n_k / (P.k_hi - P.k_lo), i)
+                      : ctl->nonfinite[i];
 }
 __device__ __forceinline__ bool kbe_skip(const kbe_problem& P, const kbe_ctl* ctl, int it) {
     if (ctl->poisoned) return true;
@@ -860,13 +874,11 @@ __device__ __forceinline__ void front_ab(const cplx* slice, int b, int f, double
 // CTAs walks the task list (tasks of both triangles, all local k).  No CTA-level
 // barriers; a 3-stage bulk-copy ring per warp keeps ~8 KB per warp in flight.
 // A converged iteration costs one tiny grid of early exits.
-__global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
-    pdl_enter();
-    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
-    if (kbe_skip(P, ctl, it)) return;
-    const double delta = coll_delta(P, ctl, it);
-    const bool incr = coll_incremental(P, ctl, n, delta);
+// The two evaluation modes are separate instantiations, so the per-slice loop carries
+// no mode branches (K2 is latency-bound per slice).
+template <bool INCR>
+__device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, int n, double delta) {
+    constexpr bool incr = INCR;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
@@ -1141,6 +1153,16 @@ __global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_proble
             __threadfence();
         }
     }
+}
+
+__global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
+    pdl_enter();
+    kbe_ctl* ctl = (kbe_ctl*)P.ctl;
+    if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
+    if (kbe_skip(P, ctl, it)) return;
+    const double delta = coll_delta(P, ctl, it);
+    if (coll_incremental(P, ctl, n, delta)) coll_body<true>(P, ctl, n, delta);
+    else coll_body<false>(P, ctl, n, delta);
 }
 
 // K2, limit_mode = "langreth" (collision.py:188-191, 211-219): the second term's
@@ -1588,13 +1610,30 @@ static size_t upd_smem_bytes(int nkl, int ppc) {
                            + (size_t)6 * nkl * 4);            // sC, sRow, sCol, sX, sY, sZ
 }
 
+// complex64 shadow of entry (planes c, 4+c; point b) of the final slice s, G and Sigma
+__device__ __noinline__ void write_shadow(const cplx* g_hist, const cplx* s_hist, float2* g_sh, float2* s_sh,
+                                         int64_t tri, int kl, int s, int c, int b) {
+    const int64_t so = (int64_t)kl * tri + slice_off(s);
+    const cplx* gp = g_hist + so;
+    const cplx* sp = s_hist + so;
+    float2* gsh = g_sh + so;
+    float2* ssh = s_sh + so;
+    for (int h = 0; h < 2; ++h) {
+        const int64_t e = sl_idx(4 * h + c, b);
+        gsh[e] = make_float2((float)gp[e].x, (float)gp[e].y);
+        ssh[e] = make_float2((float)sp[e].x, (float)sp[e].y);
+    }
+}
+
 // k-sharded publication of one frontier entry (plane c, point b) of local k kl:
 // the NCCL send buffer, or straight into every peer's buffer for data epoch e
 __device__ __forceinline__ void publish_entry(const kbe_problem& P, int kl, int c, int b, cplx v, int64_t pm,
                                               unsigned long long e) {
     const int64_t off = (int64_t)kl * 8 * pm + sl_idx(c, b);
     if (P.p2p_world > 1) {
-        for (int r = 0; r < P.p2p_world; ++r) p2p_dst(P, r, e)[off] = v;
+#pragma unroll
+        for (int r = 0; r < KBE_MAX_RANKS; ++r)
+            if (r < P.p2p_world) p2p_dst(P, r, e)[off] = v;
     } else if (P.front_send) {
         ((cplx*)P.front_send)[off] = v;
     }
@@ -1603,14 +1642,19 @@ __device__ __forceinline__ void publish_entry(const kbe_problem& P, int kl, int 
 __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail& t, unsigned long long e) {
     const int64_t off = front_chunk(P) - KBE_TAIL_CPLX;
     if (P.p2p_world > 1) {
-        for (int r = 0; r < P.p2p_world; ++r) *(KbeTail*)(p2p_dst(P, r, e) + off) = t;
+#pragma unroll
+        for (int r = 0; r < KBE_MAX_RANKS; ++r)
+            if (r < P.p2p_world) *(KbeTail*)(p2p_dst(P, r, e) + off) = t;
         p2p_signal(P, e);
     } else if (P.front_send) {
         *(KbeTail*)((cplx*)P.front_send + off) = t;
     }
 }
 
-template <int LANG>
+// INC: the problem has incremental collision evaluations (g_sh): K3 may add delta
+// slots and the predictor writes the history shadow.  A separate instantiation keeps
+// that code out of the plain kernel's registers.
+template <int LANG, int INC>
 __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC,
                                                      cudaGraphConditionalHandle next_iter) {
     pdl_enter();
@@ -1697,7 +1741,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         constexpr int UPD_BATCH = KBE_UPD_BATCH;
         cplx a = cz(), g = cz();
         // after an incremental evaluation every slot is base + delta (collision_kernel)
-        const bool dl = !LANG && ((const volatile kbe_ctl*)ctl)->incr_last;
+        const bool dl = INC && !LANG && ((const volatile kbe_ctl*)ctl)->incr_last;
         const cplx* rowD = dl ? (const cplx*)P.row_delta + rb : nullptr;
         const cplx* colD = dl ? (const cplx*)P.col_delta + cb : nullptr;
         const cplx* gcD = dl ? (const cplx*)P.gc_delta + rb : nullptr;
@@ -1804,18 +1848,9 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
             fin = fin && isfinite(row.x) && isfinite(row.y) && isfinite(col.x) && isfinite(col.y);
         }
         if (b == n - 1) { sRow[kl * 4 + c] = row; sCol[kl * 4 + c] = col; }
-        if (P.g_sh && phase == 0) {      // slice n-1 is final (G and Sigma): complex64 shadow
-            const int64_t so = (int64_t)kl * P.tri + slice_off(n - 1);
-            const cplx* sp = (const cplx*)P.s_hist + so;
-            float2* gsh = (float2*)P.g_sh + so;
-            float2* ssh = (float2*)P.s_sh + so;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t e = sl_idx(4 * h + c, b);
-                gsh[e] = make_float2((float)prev[e].x, (float)prev[e].y);
-                ssh[e] = make_float2((float)sp[e].x, (float)sp[e].y);
-            }
-        }
+        if (INC && phase == 0)   // slice n-1 is final: complex64 shadow
+            write_shadow((const cplx*)P.g_hist, (const cplx*)P.s_hist, (float2*)P.g_sh, (float2*)P.s_sh, P.tri, kl,
+                         n - 1, c, b);
         cur[sl_idx(c, b)] = row;
         cur[sl_idx(4 + c, b)] = col;
         publish_entry(P, kl, c, b, row, pm, e_next);
@@ -2042,7 +2077,9 @@ __global__ void p2p_publish_kernel(kbe_problem P) {
     const cplx* src = (const cplx*)P.front_send;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chunk; i += (int64_t)gridDim.x * blockDim.x) {
         const cplx v = src[i];
-        for (int r = 0; r < P.p2p_world; ++r) p2p_dst(P, r, e)[i] = v;
+#pragma unroll
+        for (int r = 0; r < KBE_MAX_RANKS; ++r)
+            if (r < P.p2p_world) p2p_dst(P, r, e)[i] = v;
     }
     __threadfence_system();
     __syncthreads();
@@ -2213,8 +2250,9 @@ static int ensure_attrs() {
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
     {
-        void (*upd[2])(kbe_problem, int, int, int, int, cudaGraphConditionalHandle) = {update_kernel<0>, update_kernel<1>};
-        for (int i = 0; i < 2; ++i) {
+        void (*upd[3])(kbe_problem, int, int, int, int, cudaGraphConditionalHandle) = {
+            update_kernel<0, 0>, update_kernel<1, 0>, update_kernel<0, 1>};
+        for (int i = 0; i < 3; ++i) {
             e = cudaFuncSetAttribute(upd[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(update)", e); return KBE_ERR_CUDA; }
         }
@@ -2280,8 +2318,9 @@ static void spec_update(KSpec& s, const kbe_problem* p, int n, int phase, int it
     const int nkl = p->k_hi - p->k_lo, ppc = upd_ppc(nkl, n);
     const dim3 grid((n + ppc - 1) / ppc), block(upd_threads(nkl, ppc));
     const size_t smem = upd_smem_bytes(nkl, ppc);
-    if (p->limit_mode) make_spec(s, update_kernel<1>, grid, block, smem, *p, n, phase, it, ppc, next);
-    else make_spec(s, update_kernel<0>, grid, block, smem, *p, n, phase, it, ppc, next);
+    if (p->limit_mode) make_spec(s, update_kernel<1, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else if (p->g_sh) make_spec(s, update_kernel<0, 1>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else make_spec(s, update_kernel<0, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
 }
 static void spec_hf(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
     make_spec(s, hf_mean_kernel, dim3(1), dim3(128), 0, *p, n, phase, it);

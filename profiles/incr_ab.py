@@ -64,7 +64,7 @@ def main():
 
     nk = cfgw["n_k"]
     full_b = 64.0 * nk * ((n + 1) * (n + 2) + n * (n + 1))
-    incr_b = 32.0 * nk * (n * (n + 1) + n * (n + 1)) + 64.0 * nk * (n + 1)   # shadow + FP64 slice n
+    incr_b = nk * (64.0 * n * (n + 1) + 128.0 * (n + 1))   # complex64 shadow of slices < n + FP64 slice n
     out = {"workload": args.workload, "n": n, "lib": os.environ.get("KBE_LIB", "product")}
     out["full_us"] = timed(1e-3)
     out["incr_us"] = timed(2e-9)   # > eps (not converged); 23 launches accumulate 4.6e-8 <= KBE_INCR_MAX_DELTA
