@@ -303,8 +303,8 @@ class _PeerExchange:
 def _incremental_default(n_k: int) -> bool:
     """Incremental collision evaluations (collision_kernel): KBE_INCR=1/0 forces them on /
     off; by default on for n_k >= 32, where K2 has enough tasks per launch to be closer
-    to HBM-bound and half-byte evaluations pay (profiles/r01/incr_ab_v17.jsonl: cfg3
-    +3.6 %, cfg2 -0.7 %)."""
+    to HBM-bound and half-byte evaluations pay (profiles/r01/incr_ab_v18.jsonl: cfg3
+    +2.9 %, cfg5 +0 %, cfg2 -2.3 %)."""
     env = os.environ.get("KBE_INCR")
     if env in ("0", "1"):
         return env == "1"
