@@ -22,7 +22,7 @@ TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
 TAIL_CPLX = 16     # per-rank control tail of the all-gather chunk (KBE_TAIL_CPLX)
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -47,7 +47,7 @@ class KbeProblem(ctypes.Structure):
         ("ctl", _p), ("reports", _p), ("phi", _p),
         ("row_part_g", _p), ("col_part_g", _p), ("lc_part", _p), ("gc_part_c", _p), ("lc_part_c", _p),
         ("g_sh", _p), ("s_sh", _p), ("v_prev", _p), ("fcol_part", _p),
-        ("row_delta", _p), ("col_delta", _p), ("gc_delta", _p),
+        ("row_delta", _p), ("col_delta", _p), ("gc_delta", _p), ("i_red", _p), ("g_red", _p),
         ("p2p_world", _i32), ("p2p_rank", _i32), ("p2p_local", _p), ("p2p_peers", _p * 8),
     ]
 

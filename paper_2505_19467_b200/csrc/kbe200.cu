@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <utility>
 
 #include "../../include/kbe200.h"
@@ -29,7 +30,7 @@
 #define KBE_COLL_EXP 0
 #endif
 
-#define KBE_ABI_VERSION 8
+#define KBE_ABI_VERSION 9
 
 typedef double2 cplx;
 
@@ -1651,10 +1652,69 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
     }
 }
 
+// K3a (split K3, as-printed with many local k): the fixed-order partial sums of K3's
+// phase A as a separate light kernel, one thread per (k, point, block entry), so that
+// the latency-bound sums run at full occupancy instead of under K3's register budget.
+//   a(b) = sum_{bc <= b/TB} row[bc][b] + sum_{b/ts <= sc <= nf/ts} col[sc][b] (+ fcol[b], b < nf)
+//   g(b) = sum_{bc <= b/TB} gc[bc][b]                                         (b < nf)
+// (+ the delta slots after an incremental evaluation); points 0..n-1, and n itself in
+// the corrector (the diagonal's I<(t_n, t_n)).
+template <int INC>
+__global__ void __launch_bounds__(256, 4) reduce_kernel(kbe_problem P, int n, int phase, int it) {
+    pdl_enter();
+    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(P, ctl, it)) return;
+    const int nkl = P.k_hi - P.k_lo;
+    const int64_t N1 = P.n_steps + 1, cs = N1 * 4;
+    const int nf = phase == 0 ? n - 1 : n;
+    const int npts = phase == 0 ? n : n + 1;
+    const int cts = coll_ts(nf, nkl, 0);
+    const bool dl = INC && ((const volatile kbe_ctl*)ctl)->incr_last;
+    const int64_t total = (int64_t)nkl * npts * 4;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(idx & 3), b = (int)((idx >> 2) % npts), kl = (int)((idx >> 2) / npts);
+        const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
+        const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
+        const cplx* rowP = (const cplx*)P.row_part + rb;
+        const cplx* colP = (const cplx*)P.col_part + cb;
+        const cplx* gcP = (const cplx*)P.gc_part + rb;
+        const cplx* rowD = dl ? (const cplx*)P.row_delta + rb : nullptr;
+        const cplx* colD = dl ? (const cplx*)P.col_delta + cb : nullptr;
+        const cplx* gcD = dl ? (const cplx*)P.gc_delta + rb : nullptr;
+        const int c0 = b / cts;
+        const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
+        const int na = nr + ns, ng = b < nf ? nr : 0;
+        constexpr int BATCH = 4;
+        cplx a = cz(), g = cz();
+        for (int i0 = 0; i0 < na; i0 += BATCH) {
+            cplx va[BATCH], vg[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int q = i0 + u;
+                va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
+                vg[u] = q < ng ? gcP[q * cs] : cz();
+                if (INC && dl) {
+                    if (q < na) va[u] = cadd(va[u], q < nr ? rowD[q * cs] : colD[(c0 + q - nr) * cs]);
+                    if (q < ng) vg[u] = cadd(vg[u], gcD[q * cs]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                if (i0 + u < na) a = cadd(a, va[u]);
+                if (i0 + u < ng) g = cadd(g, vg[u]);
+            }
+        }
+        if (b < nf) a = cadd(a, ((const cplx*)P.fcol_part)[((int64_t)kl * N1 + b) * 4 + c]);
+        ((cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c] = a;
+        ((cplx*)P.g_red)[((int64_t)kl * N1 + b) * 4 + c] = g;
+    }
+}
+
 // INC: the problem has incremental collision evaluations (g_sh): K3 may add delta
 // slots and the predictor writes the history shadow.  A separate instantiation keeps
 // that code out of the plain kernel's registers.
-template <int LANG, int INC>
+template <int LANG, int INC, int RED>
 __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int phase, int it, int PPC,
                                                      cudaGraphConditionalHandle next_iter) {
     pdl_enter();
@@ -1725,7 +1785,15 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     }
 
     // ---- phase A: fixed-order partial sums -------------------------------------------
-    if (own) {
+    if (RED) {
+        // split K3: reduce_kernel (K3a) already summed the partials
+        if (own) {
+            sA[(o * nkl + kl) * 4 + c] = ((const cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c];
+            sB[(o * nkl + kl) * 4 + c] = ((const cplx*)P.g_red)[((int64_t)kl * N1 + b) * 4 + c];
+        }
+        if (diag_cta && phase == 1)
+            for (int i = tid; i < nkl * 4; i += T) sC[i] = ((const cplx*)P.i_red)[((int64_t)(i >> 2) * N1 + n) * 4 + (i & 3)];
+    } else if (own) {
         // row chunks bc = 0 .. b/TB, then column chunks b/ts .. nf/ts (langreth: ts = TB)
         const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;   // [k][chunk][point][4]
         const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
@@ -1768,7 +1836,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         sA[(o * nkl + kl) * 4 + c] = a;
         sB[(o * nkl + kl) * 4 + c] = g;
     }
-    if (diag_cta) {
+    if (diag_cta && !RED) {
         if (LANG) {
             // langreth: I> rows and I< columns are independent of I< rows / I> columns
             for (int k2 = tid; k2 < nkl; k2 += T) {
@@ -2250,9 +2318,10 @@ static int ensure_attrs() {
     if (e != cudaSuccess || occ < 1) { set_err("cudaOccupancyMaxActiveBlocksPerMultiprocessor(collision)", e); return KBE_ERR_CUDA; }
     g_coll_occ = occ;
     {
-        void (*upd[3])(kbe_problem, int, int, int, int, cudaGraphConditionalHandle) = {
-            update_kernel<0, 0>, update_kernel<1, 0>, update_kernel<0, 1>};
-        for (int i = 0; i < 3; ++i) {
+        void (*upd[5])(kbe_problem, int, int, int, int, cudaGraphConditionalHandle) = {
+            update_kernel<0, 0, 0>, update_kernel<1, 0, 0>, update_kernel<0, 1, 0>, update_kernel<0, 0, 1>,
+            update_kernel<0, 1, 1>};
+        for (int i = 0; i < 5; ++i) {
             e = cudaFuncSetAttribute(upd[i], cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
             if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(update)", e); return KBE_ERR_CUDA; }
         }
@@ -2314,13 +2383,31 @@ static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
     const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
     make_spec(s, collision_kernel, dim3((int)(total < cap ? total : cap)), dim3(32), sizeof(CollSmem), *p, n, it);
 }
-static void spec_update(KSpec& s, const kbe_problem* p, int n, int phase, int it, cudaGraphConditionalHandle next) {
+// K3 split into K3a (reduce_kernel) + K3b for as-printed problems with many local k,
+// where the partial sums dominate K3 (KBE_SPLIT_MIN_K local k-points and up)
+#ifndef KBE_SPLIT_MIN_K
+#define KBE_SPLIT_MIN_K 32
+#endif
+static bool upd_split(const kbe_problem* p) {
+    return !p->limit_mode && p->i_red && p->g_red && (p->k_hi - p->k_lo) >= KBE_SPLIT_MIN_K;
+}
+static void spec_reduce(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
+    const int64_t total = (int64_t)(p->k_hi - p->k_lo) * (phase == 0 ? n : n + 1) * 4;
+    const int64_t cap = (int64_t)g_num_sms * 8;
+    const dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, cap));
+    if (p->g_sh) make_spec(s, reduce_kernel<1>, grid, dim3(256), 0, *p, n, phase, it);
+    else make_spec(s, reduce_kernel<0>, grid, dim3(256), 0, *p, n, phase, it);
+}
+static void spec_update(KSpec& s, const kbe_problem* p, int n, int phase, int it, cudaGraphConditionalHandle next,
+                        bool red = false) {
     const int nkl = p->k_hi - p->k_lo, ppc = upd_ppc(nkl, n);
     const dim3 grid((n + ppc - 1) / ppc), block(upd_threads(nkl, ppc));
     const size_t smem = upd_smem_bytes(nkl, ppc);
-    if (p->limit_mode) make_spec(s, update_kernel<1, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
-    else if (p->g_sh) make_spec(s, update_kernel<0, 1>, grid, block, smem, *p, n, phase, it, ppc, next);
-    else make_spec(s, update_kernel<0, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
+    if (p->limit_mode) make_spec(s, update_kernel<1, 0, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else if (red && p->g_sh) make_spec(s, update_kernel<0, 1, 1>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else if (red) make_spec(s, update_kernel<0, 0, 1>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else if (p->g_sh) make_spec(s, update_kernel<0, 1, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
+    else make_spec(s, update_kernel<0, 0, 0>, grid, block, smem, *p, n, phase, it, ppc, next);
 }
 static void spec_hf(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
     make_spec(s, hf_mean_kernel, dim3(1), dim3(128), 0, *p, n, phase, it);
@@ -2614,7 +2701,12 @@ int kbe_update(const kbe_problem* p, int32_t n, int32_t phase, int32_t it, void*
     if (n < 1 || n > p->n_steps || it < 0 || it >= p->max_iter) { set_err("kbe_update: n/it", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
     KSpec s;
-    spec_update(s, p, n, phase, it, 0);
+    const bool red = upd_split(p);
+    if (red) {
+        spec_reduce(s, p, n, phase, it);
+        KBE_LAUNCH_SPEC("reduce_kernel", s);
+    }
+    spec_update(s, p, n, phase, it, 0, red);
     KBE_LAUNCH_SPEC("update_kernel", s);
     return KBE_OK;
 }

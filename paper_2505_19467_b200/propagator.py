@@ -166,6 +166,9 @@ class _Workspace:
         self.reports = torch.zeros((N1, _lib.REPORT_W), dtype=torch.float64, device=device)
         self.phi = torch.zeros((N1, kl, 4), **c128)
         self.fcol_part = torch.zeros((kl, N1, 4), **c128)
+        # K3a -> K3b hand-off of the split update (as-printed, many local k)
+        self.i_red = torch.zeros((kl, N1, 4), **c128)
+        self.g_red = torch.zeros((kl, N1, 4), **c128)
         # incremental collision evaluations (as-printed): complex64 shadows of the final
         # history slices and the frontier the last evaluation used (include/kbe200.h)
         self.g_sh = self.s_sh = self.v_prev = None
@@ -210,6 +213,7 @@ class _Workspace:
         if self.lang is not None:
             (p.row_part_g, p.col_part_g, p.lc_part, p.gc_part_c, p.lc_part_c) = [t.data_ptr() for t in self.lang]
         p.fcol_part = self.fcol_part.data_ptr()
+        p.i_red, p.g_red = self.i_red.data_ptr(), self.g_red.data_ptr()
         if self.g_sh is not None:
             p.g_sh, p.s_sh, p.v_prev = self.g_sh.data_ptr(), self.s_sh.data_ptr(), self.v_prev.data_ptr()
             p.row_delta, p.col_delta, p.gc_delta = [t.data_ptr() for t in self.deltas]
