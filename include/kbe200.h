@@ -214,7 +214,7 @@ int kbe_release(const kbe_problem* p);
 /* ---- peer-to-peer frontier exchange (k-sharded ranks) ---------------
  * Replaces the per-iteration NCCL all-gather (propagator.py's _gather_frontier) by
  * stores from the update kernel into every peer's buffer over NVLink plus epoch
- * flags.  Buffer = [2 parities][world][chunk complex] + world flags + epoch, where
+ * flags.  Buffer = [2 parities][world][chunk complex] + world flags + epoch + watchdog, where
  * chunk = k_local * 8 * plane_len(N) + 16 (slice + control tail). */
 int64_t kbe_p2p_bytes(const kbe_problem* p, int32_t world);
 /* cudaMalloc + zero a buffer and export its IPC handle (64 bytes) for the peers. */
@@ -223,6 +223,9 @@ int kbe_p2p_alloc(int64_t bytes, void** ptr_out, void* ipc_handle_out);
 int kbe_p2p_open(const void* ipc_handle, void** ptr_out);
 int kbe_p2p_close(void* ptr);
 int kbe_p2p_free(void* ptr);
+/* Synchronous 8-byte device read (the exchange buffer's watchdog word: nonzero = a
+ * peer wait timed out, value - 1 = the rank waited for). */
+int kbe_p2p_read_u64(const void* dev_ptr, void* host_out);
 /* Publish this rank's send chunk (front_send: the initial slice) to every peer at the
  * next epoch; used after kbe_init_history instead of the NCCL all-gather. */
 int kbe_p2p_publish(const kbe_problem* p, void* stream);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "kbe_p2p_close": (ctypes.c_int, [_p]),
     "kbe_p2p_free": (ctypes.c_int, [_p]),
     "kbe_p2p_publish": (ctypes.c_int, [_p, _p]),
+    "kbe_p2p_read_u64": (ctypes.c_int, [_p, _p]),
     "kbe_unpack": (ctypes.c_int, [_p, _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "kbe_pack": (ctypes.c_int, [_p, _p, _i32, _i32, _i32, _i64, _p, _p]),
 }

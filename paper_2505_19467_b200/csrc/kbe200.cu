@@ -247,16 +247,36 @@ __device__ __forceinline__ cplx* p2p_dst(const kbe_problem& P, int r, unsigned l
     return (cplx*)P.p2p_peers[r] + ((int64_t)(e & 1) * P.p2p_world + P.p2p_rank) * front_chunk(P);
 }
 // consumer side: block until every rank has published the local epoch
-__device__ __noinline__ void p2p_wait_ranks(const unsigned long long* flags, int world) {
+// Watchdog: a peer that never publishes (a crashed rank, a broken peer mapping) must not
+// hang the GPU.  After KBE_P2P_TIMEOUT_NS the waiter gives up and raises the timeout
+// word (flags[world + 1]); the host checks it and raises (propagator._PeerExchange).
+#ifndef KBE_P2P_TIMEOUT_NS
+#define KBE_P2P_TIMEOUT_NS 20000000000ull
+#endif
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __noinline__ void p2p_wait_ranks(unsigned long long* flags, int world) {
     if (threadIdx.x == 0) {
         const unsigned long long e = *(volatile const unsigned long long*)(flags + world);
+        const unsigned long long t0 = globaltimer_ns();
         for (int r = 0; r < world; ++r)
-            while (ld_acquire_sys(flags + r) < e) __nanosleep(64);
+            while (ld_acquire_sys(flags + r) < e) {
+                if (*(volatile unsigned long long*)(flags + world + 1)) return;   // already timed out
+                if (globaltimer_ns() - t0 > KBE_P2P_TIMEOUT_NS) {
+                    *(volatile unsigned long long*)(flags + world + 1) = 1ull + r;
+                    __threadfence_system();
+                    return;
+                }
+                __nanosleep(256);
+            }
     }
 }
 __device__ __forceinline__ void p2p_wait(const kbe_problem& P) {
     if (P.p2p_world <= 1) return;
-    p2p_wait_ranks(p2p_flags(P, P.p2p_local), P.p2p_world);
+    p2p_wait_ranks((unsigned long long*)p2p_flags(P, P.p2p_local), P.p2p_world);
     __syncthreads();
 }
 // producer side (one thread, after every CTA's stores were fenced): epoch + 1 everywhere
@@ -2855,6 +2875,13 @@ int kbe_p2p_close(void* ptr) {
 int kbe_p2p_free(void* ptr) {
     cudaError_t e = cudaFree(ptr);
     if (e != cudaSuccess) { set_err("kbe_p2p_free", e); return KBE_ERR_CUDA; }
+    return KBE_OK;
+}
+
+int kbe_p2p_read_u64(const void* dev_ptr, void* host_out) {
+    if (!dev_ptr || !host_out) { set_err("kbe_p2p_read_u64", cudaSuccess); return KBE_ERR_ARG; }
+    cudaError_t e = cudaMemcpy(host_out, dev_ptr, 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { set_err("kbe_p2p_read_u64", e); return KBE_ERR_CUDA; }
     return KBE_OK;
 }
 

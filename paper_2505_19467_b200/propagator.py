@@ -279,6 +279,7 @@ class _PeerExchange:
         flags = [None] * world
         dist.all_gather_object(flags, bool(ok and len(peers) == world))
         ex = cls(local.value if local.value else None, peers, rank)
+        ex.nbytes = nbytes
         if not all(flags):       # every rank falls back to NCCL together
             dist.barrier()
             ex.close()
@@ -287,6 +288,19 @@ class _PeerExchange:
         for r, ptr in enumerate(peers):
             p.p2p_peers[r] = ptr
         return ex
+
+    def check(self, nbytes: int) -> None:
+        """Raise if a peer wait timed out on this rank (the watchdog word after the epoch)."""
+        if self.local is None:
+            return
+        word = torch.empty(1, dtype=torch.int64)
+        import ctypes as _ct
+        cuda = torch.cuda
+        cuda.synchronize()
+        src = self.local + nbytes - 8
+        _lib.check(_lib.lib().kbe_p2p_read_u64(src, _ct.c_void_p(word.data_ptr())), "kbe_p2p_read_u64")
+        if int(word[0]) != 0:
+            raise RuntimeError(f"peer-to-peer exchange timed out waiting for rank {int(word[0]) - 1}")
 
     def close(self, free_local: bool = True) -> None:
         """Unmap the peers' buffers (after this rank's stream is idle).  The local buffer
@@ -495,6 +509,8 @@ class PropagationDriver:
         else:
             for n in range(n0, n1 + 1):
                 self._launch_step(n)
+        if self.p2p is not None:
+            self.p2p.check(self.p2p.nbytes)
         rows = self._reports(n0, n1)
         reports = []
         for row in rows:
