@@ -307,6 +307,36 @@ def reducers_fixture():
 CLI_CONFIG = {"n_k": 4, "dt": 0.02, "n_steps": 30, "u": 1.0, "pulse_intensity": 0.2, "pulse_center": 0.1}
 
 
+CLI_CONFIG_OPTS = {"n_k": 4, "dt": 0.02, "n_steps": 24, "u": [1.0 + 0.01 * i for i in range(25)],
+                   "pulse_intensity": 0.3, "pulse_center": 0.1, "hf_mode": "on", "quadrature": "simpson",
+                   "limit_mode": "langreth", "dipole": [0.8, 0.2], "eps_v_table": [-1.0, -1.2, -1.1, -0.9],
+                   "eps_c_table": [1.0, 1.2, 1.1, 0.9], "max_iter": 8}
+
+
+def cli_opts_fixture():
+    """`kbesolve run` with every non-default physics option (hf, Simpson, langreth,
+    tabulated U(t) and bands, complex dipole): observables and report tables."""
+    import json
+    import shutil
+    import tempfile
+    from kbesolve import cli
+    d = tempfile.mkdtemp()
+    try:
+        cfg = dict(CLI_CONFIG_OPTS, observables_path=os.path.join(d, "obs.csv"),
+                   report_path=os.path.join(d, "rep.csv"), trajectory_path=os.path.join(d, "t.kbe"))
+        with open(os.path.join(d, "run.json"), "w") as fh:
+            json.dump(cfg, fh)
+        assert cli.main(["run", "--config", os.path.join(d, "run.json")]) == 0
+        shutil.copy(os.path.join(d, "obs.csv"), os.path.join(HERE, "cli_opts_observables.csv"))
+        shutil.copy(os.path.join(d, "rep.csv"), os.path.join(HERE, "cli_opts_report.csv"))
+        shutil.copy(os.path.join(d, "t.kbe"), os.path.join(HERE, "cli_opts.kbe"))
+        with open(os.path.join(HERE, "cli_opts_config.json"), "w") as fh:
+            json.dump(CLI_CONFIG_OPTS, fh, indent=1)
+        print("wrote cli_opts.* fixtures")
+    finally:
+        shutil.rmtree(d)
+
+
 def cli_fixture():
     """`kbesolve run` on a small config: the KBE1 trajectory bytes, the observables and
     report tables (cli.py:42-87, trajio.py:27-36), and `inspect` output."""

@@ -193,3 +193,26 @@ def test_cli_bench_sweep_scaling_tables(tmp_path):
         lines = out.read_text().strip().splitlines()
         assert lines[0] == header and len(lines) >= 2
         assert all(len(ln.split(",")) == len(header.split(",")) for ln in lines)
+
+
+@pytest.mark.gpu
+def test_cli_run_all_options_matches_reference(tmp_path):
+    """hf_mode=on, Simpson, langreth, tabulated U(t) and bands, complex dipole, max_iter 8:
+    the `run` tables and the trajectory against the reference CLI's own output."""
+    cfg = json.load(open(os.path.join(GOLDEN, "cli_opts_config.json")))
+    cfg.update(trajectory_path=str(tmp_path / "t.kbe"), observables_path=str(tmp_path / "obs.csv"),
+               report_path=str(tmp_path / "rep.csv"))
+    (tmp_path / "run.json").write_text(json.dumps(cfg))
+    assert cli.main(["run", "--config", str(tmp_path / "run.json")]) == cli.EXIT_OK
+    _, ours = _parse_table(tmp_path / "obs.csv")
+    _, ref = _parse_table(os.path.join(GOLDEN, "cli_opts_observables.csv"))
+    assert ours.shape == ref.shape
+    np.testing.assert_allclose(ours[:, :4], ref[:, :4], rtol=0, atol=1e-12)
+    _, ours = _parse_table(tmp_path / "rep.csv")
+    _, ref = _parse_table(os.path.join(GOLDEN, "cli_opts_report.csv"))
+    np.testing.assert_array_equal(ours[:, 0], ref[:, 0])
+    assert np.sum(ours[:, 1] != ref[:, 1]) <= 1
+    np.testing.assert_allclose(ours[:, 4:6], ref[:, 4:6], rtol=0, atol=1e-10)
+    _, gl, gg = trajio.read_arrays(str(tmp_path / "t.kbe"))
+    _, rl, rg = trajio.read_arrays(os.path.join(GOLDEN, "cli_opts.kbe"))
+    assert rel_err(gl, rl) <= 1e-10 and rel_err(gg, rg) <= 1e-10
