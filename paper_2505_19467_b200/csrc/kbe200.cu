@@ -433,7 +433,15 @@ __host__ __device__ __forceinline__ int sigma_hp_per_block(int nk) {
     const int t = 8 * nk / sg_r(nk);
     return t >= 256 ? 1 : 256 / t;
 }
-static size_t sigma_smem_bytes(int nk) { return (size_t)sigma_hp_per_block(nk) * SgDims(nk).per * sizeof(cplx); }
+// half-pairs per CTA for a launch with `hps` half-pairs: fewer than the thread budget
+// allows when that keeps >= 2 CTAs per SM (small frontiers / small n_k are latency-bound)
+static int sigma_hb_launch(int nk, int hps, int sms) {
+    int hb = sigma_hp_per_block(nk);
+    const int t = 8 * nk / sg_r(nk);              // stage-1 tasks per half-pair
+    const int floor_hb = t >= 64 ? 1 : 64 / t;    // keep >= 64 busy threads per CTA
+    while (hb > floor_hb && (hps + hb - 1) / hb < 2 * sms) hb >>= 1;
+    return hb;
+}
 #define SIGMA_THREADS 256
 
 template <int R, int DT, int DR>
@@ -464,11 +472,11 @@ __device__ __forceinline__ void sg_corr(const cplx* __restrict__ A, int a0, cons
 // G frontier slice n for ALL k (gathered buffer on >1 rank).
 //   lesser  (primary G<(b,n), reversed G>(n,b)) -> S<(t_b,t_n) = upper planes 4..7
 //   greater (primary G>(n,b), reversed G<(b,n)) -> S>(t_n,t_b) = lower planes 0..3
-// One CTA = sigma_hp_per_block(n_k) half-pairs (pair, component); stage 1 computes
+// One CTA = HB half-pairs (pair, component; sigma_hb_launch); stage 1 computes
 // P and X (selfenergy.py:59-94 and the inner sum of 139-203), stage 2 Sigma1 and
 // Sigma2 for the local k (selfenergy.py:104-136, 139-203), Sigma = Sigma1 - Sigma2.
 template <int R>
-__global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it) {
+__global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it, int HB) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
@@ -477,7 +485,6 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
     const int nk = P.n_k;
     const SgDims D(nk);
     const int h = D.h;
-    const int HB = sigma_hp_per_block(nk);
     const int hp0 = blockIdx.x * HB;
     const int nhp = min(HB, 2 * (n + 1) - hp0);
     const int nloc = P.k_hi - P.k_lo;
@@ -2383,12 +2390,13 @@ static int check_problem(const kbe_problem* p) {
 
 // ---- launch specs of the step kernels (shared by the stream and graph paths)
 static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
-    const int hb = sigma_hp_per_block(p->n_k);
+    const int hb = sigma_hb_launch(p->n_k, 2 * (n + 1), g_num_sms);
     const dim3 grid((2 * (n + 1) + hb - 1) / hb);
+    const size_t smem = (size_t)hb * SgDims(p->n_k).per * sizeof(cplx);
     if (sg_r(p->n_k) == 4)
-        make_spec(s, sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS), sigma_smem_bytes(p->n_k), *p, n, it);
+        make_spec(s, sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS), smem, *p, n, it, hb);
     else
-        make_spec(s, sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS), sigma_smem_bytes(p->n_k), *p, n, it);
+        make_spec(s, sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS), smem, *p, n, it, hb);
 }
 static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
     const int nkl = p->k_hi - p->k_lo;
