@@ -386,6 +386,9 @@ def run_ours(args):
     # corrector iterations launch (converged ones as no-ops); graph path: only the
     # iterations that ran (the rest sit behind conditional nodes that stay off).
     per_eval = 3 if drv.interactions_on else 2
+    # K3 split into reduce + update for as-printed problems with >= 32 local k (kbe200.cu)
+    if (drv.k_hi - drv.k_lo) >= 32 and drv.cfg.limit_mode == "as-printed" and not drv.use_graph:
+        per_eval += 1
     if world == 1 and drv.use_graph:
         per_prop = int(np.sum((1 + iters) * per_eval + 1)) + 2
     else:
