@@ -307,14 +307,15 @@ __device__ __noinline__ int nonfinite_ranks(const cplx* base, int64_t chunk, int
     return f;
 }
 __device__ __forceinline__ unsigned long long res_bits(const kbe_problem& P, const kbe_ctl* ctl, int i) {
-    return sharded(P) ? res_bits_ranks(front_base(P), front_chunk(P), P.n_k / (P.k_hi - P.k_lo), i) : ctl->res[i];
+    return sharded(P) ? res_bits_ranks(front_base(P), front_chunk(P), P.n_k / (P.k_hi - P.k_lo), i)
+                      : ((const volatile unsigned long long*)ctl->res)[i];
 }
 __device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl* ctl, int i) {
     return sharded(P) ? nonfinite_ranks(front_base(P), front_chunk(P), P.n_k / (P.k_hi - P.k_lo), i)
                       : ctl->nonfinite[i];
 }
 __device__ __forceinline__ bool kbe_skip(const kbe_problem& P, const kbe_ctl* ctl, int it) {
-    if (ctl->poisoned) return true;
+    if (*(const volatile int*)&ctl->poisoned) return true;
     for (int i = 0; i < it; ++i)
         if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) return true;
     return false;
@@ -668,9 +669,9 @@ __global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const 
 __device__ __forceinline__ void load_cell(const cplx* base, int b, cplx* lo, cplx* up) {
     base += sl_idx(0, b);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) lo[c] = __ldg(base + 32 * c);
+    for (int c = 0; c < 4; ++c) lo[c] = __ldcg(base + 32 * c);   // L2: valid before griddepcontrol.wait
 #pragma unroll
-    for (int c = 0; c < 4; ++c) up[c] = __ldg(base + 32 * (4 + c));
+    for (int c = 0; c < 4; ++c) up[c] = __ldcg(base + 32 * (4 + c));
 }
 
 // ---- TMA bulk copies + mbarriers (sm_90+ async proxy), one pipeline per warp
@@ -739,6 +740,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #endif
 #ifndef KBE_COLL_MINB
 #define KBE_COLL_MINB 16
+#endif
+#ifndef KBE_NO_EARLY
+#define KBE_NO_EARLY 0   // 1: K2 always waits for K1 at entry (A/B switch)
 #endif
 #ifndef KBE_COLL_TASKS
 #define KBE_COLL_TASKS 16384
@@ -905,7 +909,7 @@ __device__ __forceinline__ void front_ab(const cplx* slice, int b, int f, double
 // The two evaluation modes are separate instantiations, so the per-slice loop carries
 // no mode branches (K2 is latency-bound per slice).
 template <bool INCR>
-__device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, int n, double delta) {
+__device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, int n, double delta, bool& waited) {
     constexpr bool incr = INCR;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
@@ -957,6 +961,10 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
         const int wb0 = bc * TB;            // wb0 <= s0: every slice has lane 0 valid
         const int m = s1 - s0 + 1;
         const int b = wb0 + lane;
+        if (!waited && (part == 1 || s1 == n)) {   // this task reads Sigma slice n (early start)
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
         // frontier slice n (vector), its value at the previous evaluation, the streamed triangle
@@ -1183,14 +1191,29 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
     }
 }
 
+// Early start (one rank, Sigma on, no incremental evaluations): K2's only input from
+// the kernel before it (K1) is Sigma slice n.  K1 itself started only after the update
+// before it had completed, so the history, the G frontier and the convergence record
+// are final when K2's CTAs become resident: K2 skips griddepcontrol.wait at entry and
+// streams the tasks that do not touch Sigma slice n (part 0, slices < n) while K1 is
+// still running; a warp waits for K1 before its first task that does (part 1's
+// vectors, part 0's last tile row) and, at the latest, before it exits.  Pre-wait
+// reads bypass L1 (ld.cg / volatile / TMA from L2).
 __global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
-    pdl_enter();
+    const bool early = P.interacting && !P.g_sh && P.p2p_world <= 1 && !P.front_all && !KBE_NO_EARLY;
+    if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    else pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (!P.interacting) p2p_wait(P);   // first kernel after the update when Sigma is off
-    if (kbe_skip(P, ctl, it)) return;
+    if (kbe_skip(P, ctl, it)) {
+        if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
     const double delta = coll_delta(P, ctl, it);
-    if (coll_incremental(P, ctl, n, delta)) coll_body<true>(P, ctl, n, delta);
-    else coll_body<false>(P, ctl, n, delta);
+    bool waited = !early;
+    if (coll_incremental(P, ctl, n, delta)) coll_body<true>(P, ctl, n, delta, waited);
+    else coll_body<false>(P, ctl, n, delta, waited);
+    if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // K2, limit_mode = "langreth" (collision.py:188-191, 211-219): the second term's
