@@ -935,17 +935,6 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
     }
     __syncwarp();
     const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
-    if (P.g_sh && !incr) {
-        // full evaluation: snapshot the frontier vectors (G and Sigma slice n, local k)
-        // for the incremental evaluations that may follow at this frontier
-        const int64_t per = 8 * plane_len(n), tot = (int64_t)(P.k_hi - P.k_lo) * 2 * per;
-        for (int64_t i = blockIdx.x * 32 + lane; i < tot; i += (int64_t)gridDim.x * 32) {
-            const int kl = (int)(i / (2 * per)), which = (int)((i / per) & 1);
-            const int64_t e = i % per;
-            const cplx* src = (const cplx*)(which ? P.s_hist : P.g_hist) + (int64_t)kl * P.tri + slice_off(n);
-            ((cplx*)P.v_prev)[vprev_off(P, kl, which) + e] = src[e];
-        }
-    }
     unsigned gcount = 0;   // slices consumed by this CTA so far (ring position / parity)
     for (;;) {
         // dynamic work queue: balances the half-full diagonal tasks
@@ -1170,6 +1159,22 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
             }
         }
     }
+    if (P.g_sh && !incr) {
+        // full evaluation: snapshot the frontier vectors (G and Sigma slice n, local k) for
+        // the incremental evaluations that may follow at this frontier (after the wait
+        // for K1: Sigma slice n is its output)
+        if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+        const int64_t per = 8 * plane_len(n), tot = (int64_t)(P.k_hi - P.k_lo) * 2 * per;
+        for (int64_t i = blockIdx.x * 32 + lane; i < tot; i += (int64_t)gridDim.x * 32) {
+            const int kl = (int)(i / (2 * per)), which = (int)((i / per) & 1);
+            const int64_t e = i % per;
+            const cplx* src = (const cplx*)(which ? P.s_hist : P.g_hist) + (int64_t)kl * P.tri + slice_off(n);
+            ((cplx*)P.v_prev)[vprev_off(P, kl, which) + e] = __ldcg(src + e);
+        }
+    }
     // last CTA out resets the queue for the next launch on this stream and records the
     // frontier whose partials are now in the workspace
     if (lane == 0) {
@@ -1191,7 +1196,7 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
     }
 }
 
-// Early start (one rank, Sigma on, no incremental evaluations): K2's only input from
+// Early start (one rank, Sigma on): K2's only input from
 // the kernel before it (K1) is Sigma slice n.  K1 itself started only after the update
 // before it had completed, so the history, the G frontier and the convergence record
 // are final when K2's CTAs become resident: K2 skips griddepcontrol.wait at entry and
@@ -1200,7 +1205,7 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
 // vectors, part 0's last tile row) and, at the latest, before it exits.  Pre-wait
 // reads bypass L1 (ld.cg / volatile / TMA from L2).
 __global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
-    const bool early = P.interacting && !P.g_sh && P.p2p_world <= 1 && !P.front_all && !KBE_NO_EARLY;
+    const bool early = P.interacting && P.p2p_world <= 1 && !P.front_all && !KBE_NO_EARLY;
     if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
