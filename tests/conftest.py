@@ -14,6 +14,22 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built extension")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    _ensure_library()
+
+
+def _ensure_library():
+    """Build libkbe200.so (nvcc, sm_100a) when it is missing or older than its sources, so a
+    fresh checkout runs the suite; on a GPU box the prebuilt library travels in-tree."""
+    pkg = os.path.join(ROOT, "paper_2505_19467_b200")
+    lib = os.path.join(pkg, "libkbe200.so")
+    srcs = [os.path.join(pkg, "csrc", "kbe200.cu"), os.path.join(ROOT, "include", "kbe200.h")]
+    if os.path.exists(lib) and all(os.path.getmtime(lib) >= os.path.getmtime(x) for x in srcs):
+        return
+    import shutil
+    if shutil.which("nvcc") is None and not os.path.exists("/usr/local/cuda/bin/nvcc"):
+        return   # nothing to build with: the ABI checks will report the missing library
+    import __graft_entry__
+    __graft_entry__.build()
 
 
 def rel_err(a, b):
