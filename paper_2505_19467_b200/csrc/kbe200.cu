@@ -444,6 +444,9 @@ static int sigma_hb_launch(int nk, int hps, int sms) {
     return hb;
 }
 #define SIGMA_THREADS 256
+#ifndef KBE_SIG_NT256
+#define KBE_SIG_NT256 0   // 1: always 256-thread K1 CTAs (A/B switch)
+#endif
 
 template <int R, int DT, int DR>
 __device__ __forceinline__ void sg_corr(const cplx* __restrict__ A, int a0, const cplx* __restrict__ C, int c0, int nk,
@@ -476,8 +479,10 @@ __device__ __forceinline__ void sg_corr(const cplx* __restrict__ A, int a0, cons
 // One CTA = HB half-pairs (pair, component; sigma_hb_launch); stage 1 computes
 // P and X (selfenergy.py:59-94 and the inner sum of 139-203), stage 2 Sigma1 and
 // Sigma2 for the local k (selfenergy.py:104-136, 139-203), Sigma = Sigma1 - Sigma2.
-template <int R>
-__global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_problem P, int n, int it, int HB) {
+// NT threads per CTA: 256, or 128 when the launch's half-pairs per CTA need no more
+// (small n_k): no idle half of the CTA, twice the CTAs per SM
+template <int R, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT) sigma_frontier_kernel(kbe_problem P, int n, int it, int HB) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
     }
     // stage 0: V1 = G<(b,n) = -L(n,b)^dag (b<n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
     // comp 0: gp = V1, gr = V2;  comp 1: gp = V2, gr = V1 (each half-pair loads both).
-    for (int i = tid; i < nhp * 8 * nk; i += SIGMA_THREADS) {
+    for (int i = tid; i < nhp * 8 * nk; i += NT) {
         const int p = i % nhp, c = (i / nhp) & 7, k = i / (nhp * 8);
         const int hp = hp0 + p, b = hp >> 1, comp = hp & 1;
         const int cc = c & 3;
@@ -525,7 +530,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
 
     // stage 1: P_jm(q) (f < 4) and X_jm(d) (f >= 4), R consecutive outputs per task
     const int NB = nk / R;
-    for (int task = tid; task < nhp * 8 * NB; task += SIGMA_THREADS) {
+    for (int task = tid; task < nhp * 8 * NB; task += NT) {
         const int p = task / (8 * NB), f = (task / NB) & 7, blk = task % NB;
         cplx* base = sm + (int64_t)p * D.per;
         const cplx* DG = base;
@@ -557,7 +562,7 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_frontier_kernel(kbe_pr
     const double inv2 = 1.0 / ((double)nk * (double)nk);
     cplx s2v[R];
     int s2_task = -1;
-    for (int task = tid; task < nhp * 8 * NBL; task += SIGMA_THREADS) {
+    for (int task = tid; task < nhp * 8 * NBL; task += NT) {
         const int p = task / (8 * NBL), which = (task / (4 * NBL)) & 1, jm = (task / NBL) & 3, blk = task % NBL;
         const int hp = hp0 + p, b = hp >> 1;
         cplx* base = sm + (int64_t)p * D.per;
@@ -2357,9 +2362,13 @@ static int ensure_attrs() {
     if (g_attr_done) return KBE_OK;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(sigma_frontier_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(sigma_frontier_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        e = cudaFuncSetAttribute(sigma_frontier_kernel<2, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(sigma_frontier_kernel<4, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(sigma_frontier_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
@@ -2421,10 +2430,18 @@ static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
     const int hb = sigma_hb_launch(p->n_k, 2 * (n + 1), g_num_sms);
     const dim3 grid((2 * (n + 1) + hb - 1) / hb);
     const size_t smem = (size_t)hb * SgDims(p->n_k).per * sizeof(cplx);
-    if (sg_r(p->n_k) == 4)
-        make_spec(s, sigma_frontier_kernel<4>, grid, dim3(SIGMA_THREADS), smem, *p, n, it, hb);
-    else
-        make_spec(s, sigma_frontier_kernel<2>, grid, dim3(SIGMA_THREADS), smem, *p, n, it, hb);
+    // stage-1 tasks of the CTA (8 n_k / R per half-pair) and stage-2 tasks (8 NBL) fit 128 threads?
+    const int R = sg_r(p->n_k), nkl = p->k_hi - p->k_lo;
+    // (n_k >= 8: for the dimer-sized problems the 256-thread CTAs measured faster)
+    const bool small = p->n_k >= 8 && hb * 8 * (p->n_k / R) <= 128 && hb * 8 * ((nkl + R - 1) / R) <= 128 &&
+                       !KBE_SIG_NT256;
+    if (R == 4) {
+        if (small) make_spec(s, sigma_frontier_kernel<4, 128>, grid, dim3(128), smem, *p, n, it, hb);
+        else make_spec(s, sigma_frontier_kernel<4, 256>, grid, dim3(256), smem, *p, n, it, hb);
+    } else {
+        if (small) make_spec(s, sigma_frontier_kernel<2, 128>, grid, dim3(128), smem, *p, n, it, hb);
+        else make_spec(s, sigma_frontier_kernel<2, 256>, grid, dim3(256), smem, *p, n, it, hb);
+    }
 }
 static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
     const int nkl = p->k_hi - p->k_lo;
