@@ -6,9 +6,13 @@
 // device-side convergence so that a step never waits on the host.
 //
 //   K1 sigma_frontier_kernel   second-Born Sigma slice (selfenergy.py:59-325)
-//   K2 collision_kernel        history-streaming I< / I> (collision.py:141-277)
-//   K3 update_kernel           predictor / corrector / residual (propagator.py:77-226)
+//   K2 collision_kernel        history-streaming I< / I> (collision.py:141-277), full or
+//                              incremental (complex64 shadow) evaluations
+//      collision_langreth_kernel  the same for limit_mode="langreth"
+//   K3 update_kernel           predictor / corrector / residual (propagator.py:77-226);
+//      reduce_kernel           its partial sums as a separate pass for many local k
 //   K4 finish_kernel           observables, finite check, StepReport row
+//   k-sharded ranks exchange the new frontier slice peer-to-peer from K3 (kbe_p2p_*).
 //
 // All arithmetic is FP64 / complex128.  There is no CPU fallback.
 
@@ -909,7 +913,7 @@ __device__ __forceinline__ void front_ab(const cplx* slice, int b, int f, double
 
 // One warp = one task of 32 history points x ts slices; a persistent grid of 1-warp
 // CTAs walks the task list (tasks of both triangles, all local k).  No CTA-level
-// barriers; a 3-stage bulk-copy ring per warp keeps ~8 KB per warp in flight.
+// barriers; a KBE_STAGES-deep ring of 4 KB bulk copies per warp (2 stages: 16 warps/SM).
 // A converged iteration costs one tiny grid of early exits.
 // The two evaluation modes are separate instantiations, so the per-slice loop carries
 // no mode branches (K2 is latency-bound per slice).
