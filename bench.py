@@ -361,10 +361,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         _barrier(world)
         t0.record(st)
+        spec_launches = 0
         for _ in range(args.steps):
             _reset(kb, drv)
             n1 = N
-            if drv._device_sequenced():
+            if drv._speculative():      # the path driver.run() takes (speculative iteration counts)
+                drv._run_speculative(1, n1)
+                spec_launches += drv.spec_launches + 2   # + kbe_init_history's 2 kernels
+            elif drv._device_sequenced():
                 _lib.check(_lib.lib().kbe_run(drv.ws.problem_ptr(), 1, n1, drv.use_graph if world == 1 else 0,
                                               int(st.cuda_stream)))
             else:
@@ -393,9 +397,10 @@ def run_ours(args):
         per_prop = int(np.sum((1 + iters) * per_eval + 1)) + 2
     else:
         per_prop = N * ((1 + cfg.max_iter) * per_eval + 1) + 2
-    gpu_launches = args.steps * per_prop
+    gpu_launches = spec_launches if drv._speculative() else args.steps * per_prop
 
-    launch_mode = "cuda-graph (conditional corrector)" if (world == 1 and drv.use_graph) else "stream"
+    launch_mode = ("cuda-graph (conditional corrector)" if (world == 1 and drv.use_graph) else
+                   "stream, speculative iteration counts" if drv._speculative() else "stream")
     roof, cpu = None, None
     if rank == 0 and world == 1:
         roof, _ = _collision_roofline(kb, drv, hbm_peak)

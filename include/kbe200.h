@@ -208,6 +208,16 @@ int kbe_step(const kbe_problem* p, int32_t n, void* stream);
  * is launched after convergence.  Results are bitwise identical either way. */
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream);
 
+/* Speculative iteration counts (PropagationDriver.run, one rank): steps n_first..n_last
+ * launching only m <= max_iter corrector iterations each.  A step still unconverged
+ * after m sets the control block's needs_more word (offset kbe_ctl_needs_more_offset())
+ * to its index and every later launch becomes a no-op; kbe_resume_step(n, m) clears
+ * the word and runs iterations m..max_iter-1 and the finish of step n, after which the
+ * host continues from n+1.  Results equal kbe_run's bitwise. */
+int kbe_run_iters(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t m, void* stream);
+int kbe_resume_step(const kbe_problem* p, int32_t n, int32_t m_done, void* stream);
+int64_t kbe_ctl_needs_more_offset(void);
+
 /* Drop the step graph cached for this problem's control block (driver teardown). */
 int kbe_release(const kbe_problem* p);
 

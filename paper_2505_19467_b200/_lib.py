@@ -22,7 +22,7 @@ TILE_S = 32
 COL_CHUNK = 8
 REPORT_W = 24
 TAIL_CPLX = 16     # per-rank control tail of the all-gather chunk (KBE_TAIL_CPLX)
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -74,6 +74,9 @@ SIGNATURES = {
     "kbe_step": (ctypes.c_int, [_p, _i32, _p]),
     "kbe_run": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_release": (ctypes.c_int, [_p]),
+    "kbe_run_iters": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
+    "kbe_resume_step": (ctypes.c_int, [_p, _i32, _i32, _p]),
+    "kbe_ctl_needs_more_offset": (_i64, []),
     "kbe_p2p_bytes": (_i64, [_p, _i32]),
     "kbe_p2p_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(_p), _p]),
     "kbe_p2p_open": (ctypes.c_int, [_p, ctypes.POINTER(_p)]),

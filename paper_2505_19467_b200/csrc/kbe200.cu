@@ -17,6 +17,7 @@
 // All arithmetic is FP64 / complex128.  There is no CPU fallback.
 
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -34,7 +35,7 @@
 #define KBE_COLL_EXP 0
 #endif
 
-#define KBE_ABI_VERSION 9
+#define KBE_ABI_VERSION 10
 
 typedef double2 cplx;
 
@@ -43,7 +44,7 @@ struct kbe_ctl {
     unsigned long long res[KBE_MAX_ITER];  // residual bits per corrector iteration
     int nonfinite[KBE_MAX_ITER];           // frontier non-finite after iteration
     int poisoned;                          // step that produced a non-finite frontier
-    int pad;
+    int needs_more;                        // step left unconverged by a shortened launch (kbe_run_iters)
     cplx hf_sum[4];                        // k-sum of rho for hf_mode="on"
     unsigned task_next;                    // collision work queue head (reset by the last CTA)
     unsigned task_done;
@@ -197,6 +198,11 @@ __device__ __forceinline__ double quad_w(int nint, int t, double dt, int quad) {
 }
 
 // ------------------------------------------------------------------ device-side convergence
+// Every later launch is a no-op once a step poisoned the state or a shortened step
+// (kbe_run_iters) stopped unconverged; the host resumes the latter (kbe_resume_step).
+__device__ __forceinline__ bool kbe_halted(const kbe_ctl* ctl) {
+    return *(const volatile int*)&ctl->poisoned || *(const volatile int*)&ctl->needs_more;
+}
 // k-sharded ranks: every rank's all-gather chunk is its new G slice for the local k
 // followed by a 256-byte control tail (its local residual bits and non-finite flags per
 // iteration), so one all-gather per iteration also carries the convergence record and
@@ -319,7 +325,7 @@ __device__ __forceinline__ int nonfinite_at(const kbe_problem& P, const kbe_ctl*
                       : ctl->nonfinite[i];
 }
 __device__ __forceinline__ bool kbe_skip(const kbe_problem& P, const kbe_ctl* ctl, int it) {
-    if (*(const volatile int*)&ctl->poisoned) return true;
+    if (kbe_halted(ctl)) return true;
     for (int i = 0; i < it; ++i)
         if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) return true;
     return false;
@@ -1727,7 +1733,7 @@ template <int INC>
 __global__ void __launch_bounds__(256, 4) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
-    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(P, ctl, it)) return;
+    if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
     const int nkl = P.k_hi - P.k_lo;
     const int64_t N1 = P.n_steps + 1, cs = N1 * 4;
     const int nf = phase == 0 ? n - 1 : n;
@@ -1784,7 +1790,7 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
     if (phase == 0) {
-        if (ctl->poisoned) return;
+        if (kbe_halted(ctl)) return;
     } else if (kbe_skip(P, ctl, it)) {
         return;   // graph mode: next_iter keeps its default 0, so the step ends
     }
@@ -2126,7 +2132,7 @@ __global__ void phi_table_kernel(kbe_problem P, int n0, int n1, int it, int chec
 __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (phase == 0 ? ctl->poisoned != 0 : kbe_skip(P, ctl, it)) return;
+    if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
     const int nloc = P.k_hi - P.k_lo;
     if (threadIdx.x == 0) {
         cplx acc[4] = {cz(), cz(), cz(), cz()};
@@ -2157,11 +2163,12 @@ __global__ void hf_mean_kernel(kbe_problem P, int n, int phase, int it) {
 }
 
 // =================================================================== K4: finish
-__global__ void finish_kernel(kbe_problem P, int n) {
+// m_launched: corrector iterations launched for this step (< max_iter: kbe_run_iters)
+__global__ void finish_kernel(kbe_problem P, int n, int m_launched) {
     pdl_enter();
     p2p_wait(P);
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
-    if (ctl->poisoned) return;
+    if (kbe_halted(ctl)) return;
     const int nloc = P.k_hi - P.k_lo;
     __shared__ double dens[256];
     __shared__ double drift[256];
@@ -2182,8 +2189,12 @@ __global__ void finish_kernel(kbe_problem P, int n) {
     double ds = 0.0, dm = 0.0;
     for (int kl = 0; kl < nloc && kl < 256; ++kl) { ds += dens[kl]; dm = fmax(dm, drift[kl]); }
     int iters = P.max_iter, conv = 0;
-    for (int i = 0; i < P.max_iter; ++i)
+    for (int i = 0; i < m_launched; ++i)
         if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) { iters = i + 1; conv = 1; break; }
+    if (!conv && m_launched < P.max_iter) {   // more iterations needed than were launched
+        ctl->needs_more = n;
+        return;
+    }
     double* r = P.reports + (int64_t)n * KBE_REPORT_W;
     const int nonfin = nonfinite_at(P, ctl, iters - 1);
     r[0] = n;
@@ -2489,8 +2500,8 @@ static void spec_update(KSpec& s, const kbe_problem* p, int n, int phase, int it
 static void spec_hf(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
     make_spec(s, hf_mean_kernel, dim3(1), dim3(128), 0, *p, n, phase, it);
 }
-static void spec_finish(KSpec& s, const kbe_problem* p, int n) {
-    make_spec(s, finish_kernel, dim3(1), dim3(256), 0, *p, n);
+static void spec_finish(KSpec& s, const kbe_problem* p, int n, int m_launched = -1) {
+    make_spec(s, finish_kernel, dim3(1), dim3(256), 0, *p, n, m_launched < 0 ? p->max_iter : m_launched);
 }
 
 // ---- step graph (kbe_run, one rank) ---------------------------------------------------
@@ -2816,6 +2827,31 @@ int kbe_finish_step(const kbe_problem* p, int32_t n, void* stream) {
     return KBE_OK;
 }
 
+// step n with corrector iterations [it0, it1) (it0 > 0: resuming a shortened step, no
+// predictor) and the finish for `it1` launched iterations
+static int step_range(const kbe_problem* p, int n, int it0, int it1, void* stream) {
+    int rc;
+    if (it0 == 0) {
+        // Algorithm 1 (propagator.py:328-382): Sigma(n-1), I(n-1), predictor, then
+        // the corrector iterations [Sigma(n), I(n), corrector]; converged ones are no-ops.
+        if (p->interacting && (rc = kbe_sigma_frontier(p, n - 1, 0, stream))) return rc;
+        if ((rc = kbe_collision_frontier(p, n - 1, 0, stream))) return rc;
+        if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
+        if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
+    }
+    for (int it = it0; it < it1; ++it) {
+        if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
+        if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
+        if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
+        if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
+    }
+    if ((rc = ensure_attrs())) return rc;
+    KSpec s;
+    spec_finish(s, p, n, it1);
+    KBE_LAUNCH_SPEC("finish_kernel", s);
+    return KBE_OK;
+}
+
 int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
@@ -2826,20 +2862,35 @@ int kbe_step(const kbe_problem* p, int32_t n, void* stream) {
         return KBE_ERR_ARG;
     }
     if (n < 1 || n > p->n_steps) { set_err("kbe_step: n", cudaSuccess); return KBE_ERR_ARG; }
-    // Algorithm 1 (propagator.py:328-382): Sigma(n-1), I(n-1), predictor, then
-    // max_iter x [Sigma(n), I(n), corrector]; converged iterations are no-ops.
-    if (p->interacting && (rc = kbe_sigma_frontier(p, n - 1, 0, stream))) return rc;
-    if ((rc = kbe_collision_frontier(p, n - 1, 0, stream))) return rc;
-    if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
-    if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
-    for (int it = 0; it < p->max_iter; ++it) {
-        if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
-        if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
-        if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
-        if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
-    }
-    return kbe_finish_step(p, n, stream);
+    return step_range(p, n, 0, p->max_iter, stream);
 }
+
+int kbe_run_iters(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t m, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if ((sharded(*p) && p->p2p_world <= 1) || (p->p2p_world > 1 && p->hf) || m < 1 || m > p->max_iter ||
+        n_first < 1 || n_last > p->n_steps) {
+        set_err("kbe_run_iters", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    for (int n = n_first; n <= n_last; ++n)
+        if ((rc = step_range(p, n, 0, m, stream))) return rc;
+    return KBE_OK;
+}
+
+int kbe_resume_step(const kbe_problem* p, int32_t n, int32_t m_done, void* stream) {
+    int rc = check_problem(p);
+    if (rc) return rc;
+    if (n < 1 || n > p->n_steps || m_done < 1 || m_done >= p->max_iter) {
+        set_err("kbe_resume_step", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    cudaError_t e = cudaMemsetAsync((char*)p->ctl + offsetof(kbe_ctl, needs_more), 0, sizeof(int), (cudaStream_t)stream);
+    if (e != cudaSuccess) { set_err("kbe_resume_step", e); return KBE_ERR_CUDA; }
+    return step_range(p, n, m_done, p->max_iter, stream);
+}
+
+int64_t kbe_ctl_needs_more_offset(void) { return (int64_t)offsetof(kbe_ctl, needs_more); }
 
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream) {
     int rc = check_problem(p);

@@ -299,3 +299,23 @@ def test_incremental_evaluations_match_full_evaluations(name, monkeypatch):
     scale = float(a.state.hist.abs().max())
     assert float((a.state.hist - b.state.hist).abs().max()) <= 1e-13 * scale
     assert float((a.sigma.hist - b.sigma.hist).abs().max()) <= 1e-13 * float(a.sigma.hist.abs().max())
+
+
+@pytest.mark.parametrize("name", ["traj_nk16.npz", "traj_hf.npz", "traj_langreth.npz", "traj_dimer.npz"])
+def test_speculative_iteration_counts_equal_full_launches(name, monkeypatch):
+    """run() launches only as many corrector iterations as earlier steps needed and
+    resumes a step that needs more (kbe_run_iters / kbe_resume_step); the result is
+    bitwise the all-max_iter run, reports included."""
+    g = load_golden(name)
+    monkeypatch.setenv("KBE_SPECULATE", "0")
+    a = _driver_from_fixture(g)
+    ra = a.run()
+    monkeypatch.setenv("KBE_SPECULATE", "1")
+    b = _driver_from_fixture(g)
+    assert b._speculative()
+    b._spec_m = 1                      # force rollbacks at every increase
+    rb = b.run()
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    assert [r.residual_history for r in ra] == [r.residual_history for r in rb]
+    assert [r.density for r in ra] == [r.density for r in rb]
+    assert torch.equal(a.state.hist, b.state.hist) and torch.equal(a.sigma.hist, b.sigma.hist)
