@@ -417,12 +417,14 @@ class PropagationDriver:
     SPEC_CHUNK = 32
 
     def _speculative(self) -> bool:
-        """One rank, stream launches: launch only as many corrector iterations as the steps
+        """Device-sequenced stream launches: launch only as many corrector iterations as the steps
         so far needed and roll back the rare step that needs more (kbe_run_iters).  The
         no-op launches of converged iterations cost ~4 % of a cfg2 step; KBE_SPECULATE=0
         launches all max_iter iterations every step."""
-        return (self.world == 1 and not self.use_graph and self.cfg.max_iter > 1
-                and os.environ.get("KBE_SPECULATE", "1") != "0")
+        # (k-sharded peer-to-peer ranks too: every rank's finish kernel sees the same merged
+        # residuals, so all ranks stop, resume and continue at the same step)
+        return (self._device_sequenced() and not (self.world == 1 and self.use_graph)
+                and self.cfg.max_iter > 1 and os.environ.get("KBE_SPECULATE", "1") != "0")
 
     def _run_speculative(self, n0: int, n1: int) -> None:
         """Chunks of steps with m iterations each; the host reads each chunk's needs_more
