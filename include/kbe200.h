@@ -154,7 +154,8 @@ int kbe_sigma_slice(int32_t n_k, int32_t nb, const void* g_primary, const void* 
 /* ---- collision integrals (collision.py) ---------------------------------- */
 /* collision_frontier (collision.py:228-277) at step n into the partial-sum
  * workspace: row sums over the Sigma history triangle (slices 0..n) and the
- * column sums over the G history triangle (slices 0..n-1). */
+ * column sums over the G history triangle (slices 0..n-1).  Ordered after all
+ * earlier work on the stream (only the step sequencer overlaps it with Sigma). */
 int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream);
 
 /* collision_row (collision.py:141-162): the kernel-level row-slice contraction on

@@ -102,6 +102,19 @@ __device__ __forceinline__ cplx cfma_cb(cplx a, cplx b, cplx acc) {
 __device__ __forceinline__ cplx cfma_ca(cplx a, cplx b, cplx acc) {
     return make_double2(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
 }
+// complex64 (the incremental collision evaluations' arithmetic)
+typedef float2 fcx;
+__device__ __forceinline__ fcx f32(cplx a) { return make_float2((float)a.x, (float)a.y); }
+__device__ __forceinline__ cplx f64(fcx a) { return make_double2(a.x, a.y); }
+__device__ __forceinline__ fcx cfma(fcx a, fcx b, fcx acc) {
+    return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ fcx cfma_cb(fcx a, fcx b, fcx acc) {
+    return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, acc.x)), fmaf(a.y, b.x, fmaf(-a.x, b.y, acc.y)));
+}
+__device__ __forceinline__ fcx cfma_ca(fcx a, fcx b, fcx acc) {
+    return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, acc.y)));
+}
 // Smith's division
 __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
     if (fabs(b.x) >= fabs(b.y)) {
@@ -116,33 +129,37 @@ __device__ __forceinline__ cplx cmul_mi(cplx z, double dt) { return make_double2
 __device__ __forceinline__ cplx cmul_pi(cplx z, double dt) { return make_double2(-dt * z.y, dt * z.x); }
 
 // 2x2 complex blocks, row-major: m[0]=00 m[1]=01 m[2]=10 m[3]=11
+// (templates over cplx / fcx)
 // acc += A*B
-__device__ __forceinline__ void mm_acc(cplx* acc, const cplx* A, const cplx* B) {
+template <class C>
+__device__ __forceinline__ void mm_acc(C* acc, const C* A, const C* B) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            cplx t = cfma(A[2 * i], B[j], acc[2 * i + j]);
+            C t = cfma(A[2 * i], B[j], acc[2 * i + j]);
             acc[2 * i + j] = cfma(A[2 * i + 1], B[2 + j], t);
         }
 }
 // acc += A*B^dagger : (B^dag)_{kj} = conj(B_{jk})
-__device__ __forceinline__ void mm_bdag_acc(cplx* acc, const cplx* A, const cplx* B) {
+template <class C>
+__device__ __forceinline__ void mm_bdag_acc(C* acc, const C* A, const C* B) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            cplx t = cfma_cb(A[2 * i], B[2 * j], acc[2 * i + j]);
+            C t = cfma_cb(A[2 * i], B[2 * j], acc[2 * i + j]);
             acc[2 * i + j] = cfma_cb(A[2 * i + 1], B[2 * j + 1], t);
         }
 }
 // acc += A^dagger*B : (A^dag)_{ik} = conj(A_{ki})
-__device__ __forceinline__ void mm_adag_acc(cplx* acc, const cplx* A, const cplx* B) {
+template <class C>
+__device__ __forceinline__ void mm_adag_acc(C* acc, const C* A, const C* B) {
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            cplx t = cfma_ca(A[i], B[j], acc[2 * i + j]);
+            C t = cfma_ca(A[i], B[j], acc[2 * i + j]);
             acc[2 * i + j] = cfma_ca(A[2 + i], B[2 + j], t);
         }
 }
@@ -343,27 +360,28 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 // ------------------------------------------------------------------ warp reduction
-// Sum 8 doubles over the 32 lanes with a reduce-scatter butterfly (9 shuffles);
+// Sum 8 values over the 32 lanes with a reduce-scatter butterfly (9 shuffles);
 // lane L ends up holding the total of value index (L >> 2) & 7.
-__device__ __forceinline__ double warp_rs8(const double* v, int lane) {
+template <class T>
+__device__ __forceinline__ T warp_rs8(const T* v, int lane) {
     const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
-    double a[4];
+    T a[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const double send = h4 ? v[i] : v[i + 4];
-        const double keep = h4 ? v[i + 4] : v[i];
+        const T send = h4 ? v[i] : v[i + 4];
+        const T keep = h4 ? v[i + 4] : v[i];
         a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    double c[2];
+    T c[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        const double send = h3 ? a[i] : a[i + 2];
-        const double keep = h3 ? a[i + 2] : a[i];
+        const T send = h3 ? a[i] : a[i + 2];
+        const T keep = h3 ? a[i + 2] : a[i];
         c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-    const double send = h2 ? c[0] : c[1];
-    const double keep = h2 ? c[1] : c[0];
-    double d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    const T send = h2 ? c[0] : c[1];
+    const T keep = h2 ? c[1] : c[0];
+    T d = keep + __shfl_xor_sync(0xffffffffu, send, 4);
     d += __shfl_xor_sync(0xffffffffu, d, 2);
     d += __shfl_xor_sync(0xffffffffu, d, 1);
     return d;
@@ -888,20 +906,10 @@ __device__ __forceinline__ void issue_shadow(const float2* sh, int s, int wb0, c
     mbar_expect_tx(bar, 8u * 32u * 8u);
     bulk_g2s(dst[0], sh + slice_off(s) + sl_idx(0, wb0), 8u * 32u * 8u, bar, pol);
 }
-// lane's 8 planes of one stage: FP64 block or complex64 shadow block
-__device__ __forceinline__ void stage_cell(const cplx (*buf)[32], bool shadow, int lane, cplx* lo, cplx* up) {
-    if (shadow) {
-        const float2* f = reinterpret_cast<const float2*>(buf);
+// lane's 8 planes of one FP64 stage
+__device__ __forceinline__ void stage_cell(const cplx (*buf)[32], int lane, cplx* lo, cplx* up) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const float2 a = f[c * 32 + lane], b = f[(4 + c) * 32 + lane];
-            lo[c] = make_double2(a.x, a.y);
-            up[c] = make_double2(b.x, b.y);
-        }
-    } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) { lo[c] = buf[c][lane]; up[c] = buf[4 + c][lane]; }
-    }
+    for (int c = 0; c < 4; ++c) { lo[c] = buf[c][lane]; up[c] = buf[4 + c][lane]; }
 }
 // part-0 vectors at point b of the G frontier slice f: w_b A(b), w_b B(b) with
 // A(b) = G>(t_f,t_b) = -U(f,b)^dag (b < f) | U(f,f), B(b) = G<(t_f,t_b) = L(f,b)
@@ -921,11 +929,33 @@ __device__ __forceinline__ void front_ab(const cplx* slice, int b, int f, double
 // CTAs walks the task list (tasks of both triangles, all local k).  No CTA-level
 // barriers; a KBE_STAGES-deep ring of 4 KB bulk copies per warp (2 stages: 16 warps/SM).
 // A converged iteration costs one tiny grid of early exits.
-// The two evaluation modes are separate instantiations, so the per-slice loop carries
-// no mode branches (K2 is latency-bound per slice).
-template <bool INCR>
+// The two evaluation modes are separate bodies, so the per-slice loop carries no mode
+// branches (K2 is latency-bound per slice).
+
+// last CTA out resets the queue for the next launch on this stream and records the
+// frontier whose partials are now in the workspace
+__device__ __forceinline__ void coll_finish(kbe_ctl* ctl, int n, double delta, bool incr) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned d = atomicAdd(&ctl->task_done, 1u);
+        if (d == gridDim.x - 1) {
+            ctl->task_next = 0u;
+            ctl->task_done = 0u;
+            ctl->prev_f1 = n + 1;
+            if (incr) {
+                ctl->dsum += delta;
+            } else {
+                ctl->full_f1 = n + 1;
+                ctl->dsum = 0.0;
+            }
+            ctl->incr_last = incr ? 1 : 0;
+            __threadfence();
+        }
+    }
+}
+
+// full FP64 evaluation
 __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, int n, double delta, bool& waited) {
-    constexpr bool incr = INCR;
     extern __shared__ __align__(128) unsigned char smraw[];
     CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
     const int lane = threadIdx.x;
@@ -937,13 +967,8 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
     const int per_k = (tri0 + tri1) * nsub;
     const int total = per_k * (P.k_hi - P.k_lo);
     uint64_t* bars = sm.bar;
-    // The ring is latency-bound (a stage is refilled only once consumed), so its depth in
-    // slices, not bytes, sets the rate: an incremental evaluation's 2 KB shadow blocks
-    // get twice as many stages in the same shared memory.
-    const int STG = incr ? 2 * KBE_STAGES : KBE_STAGES;
-    auto stage = [&](unsigned st) -> cplx (*)[32] {
-        return reinterpret_cast<cplx (*)[32]>(reinterpret_cast<unsigned char*>(sm.buf) + st * (incr ? 2048u : 4096u));
-    };
+    constexpr int STG = KBE_STAGES;
+    auto stage = [&](unsigned st) -> cplx (*)[32] { return sm.buf[st]; };
     if (lane == 0) {
         for (int i = 0; i < STG; ++i) mbar_init(&bars[i], 1);
         mbar_fence_init();
@@ -971,51 +996,29 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
         }
         const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
         const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
-        // frontier slice n (vector), its value at the previous evaluation, the streamed triangle
+        // frontier slice n (vector) and the streamed triangle
         const cplx* fr = (part == 0 ? G : S) + slice_off(n);
-        const cplx* fp = incr ? (const cplx*)P.v_prev + vprev_off(P, kl, part) : nullptr;
         const cplx* hist = part == 0 ? S : G;
-        const float2* hsh = (const float2*)(part == 0 ? P.s_sh : P.g_sh) + (incr ? (int64_t)kl * P.tri : 0);
-        auto issue = [&](int s, unsigned st) {
-            if (incr) issue_shadow(hsh, s, wb0, stage(st), &bars[st], pol_stream);
-            else issue_slice(hist, s, wb0, stage(st), &bars[st], pol_stream);
-        };
-        // slices through the ring: all, except an incremental evaluation's slice n (FP64,
-        // read directly at the end of the task)
-        const int mr = (incr && part == 0 && s1 == n) ? m - 1 : m;
+        auto issue = [&](int s, unsigned st) { issue_slice(hist, s, wb0, stage(st), &bars[st], pol_stream); };
         __syncwarp();
         if (lane == 0)
-            for (int i = 0; i < STG && i < mr; ++i) issue(s0 + i, (gcount + i) % STG);
+            for (int i = 0; i < STG && i < m; ++i) issue(s0 + i, (gcount + i) % STG);
         double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
-        double* outD = (double*)(part == 0 ? P.row_delta : P.gc_delta);
-        // row slot (bc, s): full evaluation -> base slot; incremental -> delta slot, except
-        // for slice n, which is always full (base slot, zero delta)
+        // row slot (bc, s): the base slot (the delta slots are ignored after a full evaluation)
         auto put_row = [&](int s, double rr) {
             if (KBE_COLL_EXP != 4 && (lane & 3) == 0) {
                 const int64_t o = (((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2);
-                if (incr && s < n) {
-                    st_keep(&outD[o], rr, pol_keep);
-                } else {
-                    st_keep(&outP[o], rr, pol_keep);
-                    if (incr) st_keep(&outD[o], 0.0, pol_keep);
-                }
+                st_keep(&outP[o], rr, pol_keep);
             }
         };
 
         if (part == 0) {
-            // per-slice vectors w_s A(s), w_s B(s) (incremental: their change since the last
-            // evaluation, except for slice n itself)
+            // per-slice vectors w_s A(s), w_s B(s)
             if (lane < m) {
                 const int s = s0 + lane;
                 const double w = quad_w(n, s, dt, P.quad);
                 cplx a[4], l[4];
                 front_ab(fr, s, n, w, a, l);
-                if (incr && s < n) {
-                    cplx a0[4], l0[4];
-                    front_ab(fp, s, n, w, a0, l0);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) { a[c] = csub(a[c], a0[c]); l[c] = csub(l[c], l0[c]); }
-                }
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { sm.vec[lane][c] = a[c]; sm.vec[lane][4 + c] = l[c]; }
             }
@@ -1023,48 +1026,29 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
 #pragma unroll
             for (int c = 0; c < 4; ++c) { Ab[c] = cz(); Bb[c] = cz(); col[c] = cz(); }
             const double wb = quad_w(n, b, dt, P.quad);
-            if (b <= s1) {
-                front_ab(fr, b, n, wb, Ab, Bb);
-                if (incr) {
-                    cplx a0[4], l0[4];
-                    front_ab(fp, b, n, wb, a0, l0);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) { Ab[c] = csub(Ab[c], a0[c]); Bb[c] = csub(Bb[c], l0[c]); }
-                }
-            }
-            // column chunk slot (history part): base (full) or delta (incremental)
-            cplx* colP = (cplx*)(incr ? P.col_delta : P.col_part) + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
+            if (b <= s1) front_ab(fr, b, n, wb, Ab, Bb);
+            cplx* colP = (cplx*)P.col_part + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
             __syncwarp();
-            for (int i = 0; i < m; ++i) {
+            for (int i = 0; i < m; ++i, ++gcount) {
                 const int s = s0 + i;
-                const bool ring = i < mr;
                 const unsigned st = gcount % STG;
                 if (s == n) {
-                    // frontier slice: its column sums go to their own slot; an incremental
-                    // evaluation switches to the full vectors for it
+                    // frontier slice: its column sums go to their own slot
                     if (b <= s1) {
 #pragma unroll
                         for (int c = 0; c < 4; ++c) st_keep2(&colP[c], cneg(col[c]), pol_keep);
                     }
 #pragma unroll
                     for (int c = 0; c < 4; ++c) col[c] = cz();
-                    if (incr && b <= s1) front_ab(fr, b, n, wb, Ab, Bb);
                 }
                 cplx SL[4], SU[4];
-                if (ring) {
-                    mbar_wait(&bars[st], (gcount / STG) & 1u);
-                    stage_cell(stage(st), incr, lane, SL, SU);
-                    // the stage is in registers: refill it now, so the copy overlaps this
-                    // slice's arithmetic (proxy fence: generic reads before async writes)
-                    fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0 && i + STG < mr) issue(s + STG, st);
-                    ++gcount;
-                } else {   // incremental evaluation: slice n in FP64, straight from global
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) { SL[c] = cz(); SU[c] = cz(); }
-                    if (b <= s) load_cell(hist + slice_off(s), b, SL, SU);
-                }
+                mbar_wait(&bars[st], (gcount / STG) & 1u);
+                stage_cell(stage(st), lane, SL, SU);
+                // the stage is in registers: refill it now, so the copy overlaps this
+                // slice's arithmetic (proxy fence: generic reads before async writes)
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && i + STG < m) issue(s + STG, st);
                 cplx row[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) row[c] = cz();
@@ -1103,7 +1087,7 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
                 put_row(s, rr);
             }
             if (b <= s1) {
-                if (s1 == n) {   // slice n's column sums (full in both modes)
+                if (s1 == n) {   // slice n's column sums
                     cplx* fc = (cplx*)P.fcol_part + ((int64_t)kl * N1 + b) * 4;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) st_keep2(&fc[c], cneg(col[c]), pol_keep);
@@ -1114,25 +1098,17 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
             }
         } else {
             // column collision over the G triangle (slices < n: all history); frontier
-            // vectors X = SL(n,b), Y = SU(n,b) (incremental: their change)
+            // vectors X = SL(n,b), Y = SU(n,b)
             cplx X[4], Y[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { X[c] = cz(); Y[c] = cz(); }
-            if (b <= s1) {
-                load_cell(fr, b, X, Y);
-                if (incr) {
-                    cplx X0[4], Y0[4];
-                    load_cell(fp, b, X0, Y0);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) { X[c] = csub(X[c], X0[c]); Y[c] = csub(Y[c], Y0[c]); }
-                }
-            }
+            if (b <= s1) load_cell(fr, b, X, Y);
             for (int i = 0; i < m; ++i, ++gcount) {
                 const int j = s0 + i;
                 const unsigned st = gcount % STG;
                 mbar_wait(&bars[st], (gcount / STG) & 1u);
                 cplx GL[4], GU[4];
-                stage_cell(stage(st), incr, lane, GL, GU);
+                stage_cell(stage(st), lane, GL, GU);
                 fence_proxy_async();   // stage in registers: refill it during the arithmetic
                 __syncwarp();
                 if (lane == 0 && i + STG < m) issue(j + STG, st);
@@ -1174,9 +1150,9 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
             }
         }
     }
-    if (P.g_sh && !incr) {
-        // full evaluation: snapshot the frontier vectors (G and Sigma slice n, local k) for
-        // the incremental evaluations that may follow at this frontier (after the wait
+    if (P.g_sh) {
+        // snapshot the frontier vectors (G and Sigma slice n, local k) for the
+        // incremental evaluations that may follow at this frontier (after the wait
         // for K1: Sigma slice n is its output)
         if (!waited) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1190,25 +1166,230 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
             ((cplx*)P.v_prev)[vprev_off(P, kl, which) + e] = __ldcg(src + e);
         }
     }
-    // last CTA out resets the queue for the next launch on this stream and records the
-    // frontier whose partials are now in the workspace
+    coll_finish(ctl, n, delta, false);
+}
+
+// Incremental evaluation: the history cells (slices < n) enter only through the change
+// of the frontier vectors, M dv with |dv| <= KBE_INCR_MAX_DELTA, so they are computed in
+// complex64 straight from the complex64 shadow (FP32 FMAs, no conversions, 32-bit
+// shuffles): relative error ~2^-24 x (products + <= 32-term sums) of a term that is
+// itself <= 1e-7 of I, i.e. <= ~2e-13 |I| worst case and ~1e-14 typically.  Slice n
+// (row tasks of the last tile row) is re-evaluated in full FP64 after the loop.
+// An incremental slice is half the bytes of a full one, so FP64 arithmetic (and its
+// conversions) would bound the ring, not HBM.
+__device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ctl, int n, double delta,
+                                               bool& waited) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    CollSmem& sm = *reinterpret_cast<CollSmem*>(smraw);
+    fcx (*vec)[8] = reinterpret_cast<fcx (*)[8]>(&sm.vec[0][0]);
+    const int lane = threadIdx.x;
+    const int N1 = P.n_steps + 1;
+    const double dt = P.dt;
+    const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
+    const int tri0 = T0 * (T0 + 1) / 2, tri1 = T1 * (T1 + 1) / 2;
+    const int ts = coll_ts(n, P.k_hi - P.k_lo, 0), nsub = TS / ts;
+    const int per_k = (tri0 + tri1) * nsub;
+    const int total = per_k * (P.k_hi - P.k_lo);
+    uint64_t* bars = sm.bar;
+    // the ring is latency-bound (a stage is refilled only once consumed), so its depth in
+    // slices, not bytes, sets the rate: 2 KB shadow blocks get twice the stages
+    constexpr int STG = 2 * KBE_STAGES;
+    auto stage = [&](unsigned st) -> cplx (*)[32] {
+        return reinterpret_cast<cplx (*)[32]>(reinterpret_cast<unsigned char*>(sm.buf) + st * 2048u);
+    };
     if (lane == 0) {
-        __threadfence();
-        const unsigned d = atomicAdd(&ctl->task_done, 1u);
-        if (d == gridDim.x - 1) {
-            ctl->task_next = 0u;
-            ctl->task_done = 0u;
-            ctl->prev_f1 = n + 1;
-            if (incr) {
-                ctl->dsum += delta;
-            } else {
-                ctl->full_f1 = n + 1;
-                ctl->dsum = 0.0;
+        for (int i = 0; i < STG; ++i) mbar_init(&bars[i], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    unsigned gcount = 0;
+    for (;;) {
+        unsigned tk = 0;
+        if (lane == 0) tk = atomicAdd(&ctl->task_next, 1u);
+        const int task = (int)__shfl_sync(0xffffffffu, tk, 0);
+        if (task >= total) break;
+        const CollTask ct = coll_task(task, P.k_hi - P.k_lo, T0, T1, nsub);
+        const int kl = ct.kl, part = ct.part, sc = ct.sc, bc = ct.bc, sub = ct.sub;
+        const int smax = part == 0 ? n : n - 1;
+        const int s0 = sc * TS + sub * ts, s1 = min(s0 + ts - 1, smax);
+        if (s0 > smax) continue;
+        const int wb0 = bc * TB;
+        const int m = s1 - s0 + 1;
+        const int b = wb0 + lane;
+        if (!waited && (part == 1 || s1 == n)) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            waited = true;
+        }
+        const cplx* G = (const cplx*)P.g_hist + (int64_t)kl * P.tri;
+        const cplx* S = (const cplx*)P.s_hist + (int64_t)kl * P.tri;
+        // frontier slice n, its value at the last full evaluation, the shadow triangle
+        const cplx* fr = (part == 0 ? G : S) + slice_off(n);
+        const cplx* fp = (const cplx*)P.v_prev + vprev_off(P, kl, part);
+        const float2* hsh = (const float2*)(part == 0 ? P.s_sh : P.g_sh) + (int64_t)kl * P.tri;
+        auto issue = [&](int s, unsigned st) { issue_shadow(hsh, s, wb0, stage(st), &bars[st], pol_stream); };
+        // slices through the ring: those < n (slice n: FP64 epilogue)
+        const int mr = (part == 0 && s1 == n) ? m - 1 : m;
+        __syncwarp();
+        if (lane == 0)
+            for (int i = 0; i < STG && i < mr; ++i) issue(s0 + i, (gcount + i) % STG);
+        double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
+        double* outD = (double*)(part == 0 ? P.row_delta : P.gc_delta);
+        auto put = [&](double* out, int s, double rr) {
+            if ((lane & 3) == 0) st_keep(&out[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
+        };
+        auto shadow_cell = [&](unsigned st, fcx* lo, fcx* up) {
+            const fcx* f = reinterpret_cast<const fcx*>(stage(st));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { lo[c] = f[c * 32 + lane]; up[c] = f[(4 + c) * 32 + lane]; }
+        };
+
+        if (part == 0) {
+            // per-slice vector changes w_s dA(s), w_s dB(s) (slices < n)
+            if (lane < mr) {
+                const int s = s0 + lane;
+                const double w = quad_w(n, s, dt, P.quad);
+                cplx a[4], l[4], a0[4], l0[4];
+                front_ab(fr, s, n, w, a, l);
+                front_ab(fp, s, n, w, a0, l0);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { vec[lane][c] = f32(csub(a[c], a0[c])); vec[lane][4 + c] = f32(csub(l[c], l0[c])); }
             }
-            ctl->incr_last = incr ? 1 : 0;
-            __threadfence();
+            fcx Ab[4], Bb[4], col[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { Ab[c] = make_float2(0.f, 0.f); Bb[c] = Ab[c]; col[c] = Ab[c]; }
+            const double wb = quad_w(n, b, dt, P.quad);
+            if (b <= s1) {
+                cplx a[4], l[4], a0[4], l0[4];
+                front_ab(fr, b, n, wb, a, l);
+                front_ab(fp, b, n, wb, a0, l0);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { Ab[c] = f32(csub(a[c], a0[c])); Bb[c] = f32(csub(l[c], l0[c])); }
+            }
+            __syncwarp();
+            for (int i = 0; i < mr; ++i, ++gcount) {
+                const int s = s0 + i;
+                const unsigned st = gcount % STG;
+                mbar_wait(&bars[st], (gcount / STG) & 1u);
+                fcx SL[4], SU[4];
+                shadow_cell(st, SL, SU);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && i + STG < mr) issue(s + STG, st);
+                fcx row[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) row[c] = make_float2(0.f, 0.f);
+                if (b <= s) {
+                    mm_acc(row, Ab, SU);
+                    if (b < s) {
+                        mm_bdag_acc(row, Bb, SL);
+                        fcx As[4], Bs[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) { As[c] = vec[i][c]; Bs[c] = vec[i][4 + c]; }
+                        mm_bdag_acc(col, As, SU);
+                        mm_acc(col, Bs, SL);
+                    } else {
+                        fcx t[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) t[c] = make_float2(0.f, 0.f);
+                        mm_acc(t, Bb, SL);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) row[c] = make_float2(row[c].x - t[c].x, row[c].y - t[c].y);
+                    }
+                }
+                float v[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
+                put(outD, s, (double)warp_rs8(v, lane));
+            }
+            // history-part column sums -> the chunk's delta slot
+            if (b <= s1) {
+                cplx* colD = (cplx*)P.col_delta + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) st_keep2(&colD[c], cneg(f64(col[c])), pol_keep);
+            }
+            if (s1 == n) {
+                // slice n in FP64 with the full vectors: base row slot (zero delta), fcol slot
+                cplx SL[4], SU[4], Af[4], Bf[4], row[4], cf[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { SL[c] = cz(); SU[c] = cz(); Af[c] = cz(); Bf[c] = cz(); row[c] = cz(); cf[c] = cz(); }
+                if (b <= n) {
+                    load_cell(S + slice_off(n), b, SL, SU);
+                    front_ab(fr, b, n, wb, Af, Bf);
+                    mm_acc(row, Af, SU);
+                    if (b < n) {
+                        mm_bdag_acc(row, Bf, SL);
+                        cplx As[4], Bs[4];
+                        front_ab(fr, n, n, quad_w(n, n, dt, P.quad), As, Bs);
+                        mm_bdag_acc(cf, As, SU);
+                        mm_acc(cf, Bs, SL);
+                    } else {
+                        cplx t[4];
+                        mm(t, Bf, SL);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) row[c] = csub(row[c], t[c]);
+                    }
+                }
+                double v[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
+                const double rr = warp_rs8(v, lane);
+                put(outP, n, rr);
+                put(outD, n, 0.0);
+                if (b <= n) {
+                    cplx* fc = (cplx*)P.fcol_part + ((int64_t)kl * N1 + b) * 4;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) st_keep2(&fc[c], cneg(cf[c]), pol_keep);
+                }
+            }
+        } else {
+            // column collision over the G triangle: X = dSL(n,b), Y = dSU(n,b)
+            fcx X[4], Y[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { X[c] = make_float2(0.f, 0.f); Y[c] = X[c]; }
+            if (b <= s1) {
+                cplx x[4], y[4], x0[4], y0[4];
+                load_cell(fr, b, x, y);
+                load_cell(fp, b, x0, y0);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { X[c] = f32(csub(x[c], x0[c])); Y[c] = f32(csub(y[c], y0[c])); }
+            }
+            for (int i = 0; i < m; ++i, ++gcount) {
+                const int j = s0 + i;
+                const unsigned st = gcount % STG;
+                mbar_wait(&bars[st], (gcount / STG) & 1u);
+                fcx GL[4], GU[4];
+                shadow_cell(st, GL, GU);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0 && i + STG < m) issue(j + STG, st);
+                fcx acc[4], t[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { acc[c] = make_float2(0.f, 0.f); t[c] = acc[c]; }
+                if (b <= j) {
+                    const float w = (float)quad_w(j, b, dt, P.quad);
+                    mm_bdag_acc(t, GL, X);             // GL X^dag
+                    if (b < j) {
+                        mm_adag_acc(acc, GU, Y);       // GU^dag Y
+                    } else {
+                        fcx u[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) u[c] = make_float2(0.f, 0.f);
+                        mm_acc(u, GU, Y);
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) acc[c] = make_float2(-u[c].x, -u[c].y);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[c] = make_float2((acc[c].x - t[c].x) * w, (acc[c].y - t[c].y) * w);
+                }
+                float v[8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
+                put(outD, j, (double)warp_rs8(v, lane));
+            }
         }
     }
+    coll_finish(ctl, n, delta, true);
 }
 
 // Early start (one rank, Sigma on): K2's only input from
@@ -1218,9 +1399,12 @@ __device__ __forceinline__ void coll_body(const kbe_problem& P, kbe_ctl* ctl, in
 // streams the tasks that do not touch Sigma slice n (part 0, slices < n) while K1 is
 // still running; a warp waits for K1 before its first task that does (part 1's
 // vectors, part 0's last tile row) and, at the latest, before it exits.  Pre-wait
-// reads bypass L1 (ld.cg / volatile / TMA from L2).
-__global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it) {
-    const bool early = P.interacting && P.p2p_world <= 1 && !P.front_all && !KBE_NO_EARLY;
+// reads bypass L1 (ld.cg / volatile / TMA from L2).  `after_sigma` is set only by the
+// step sequencer (K1 is the launch before): a K2 launched on its own through
+// kbe_collision_frontier waits for all earlier work, so two back-to-back K2s never
+// share the task queue.
+__global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_problem P, int n, int it, int after_sigma) {
+    const bool early = after_sigma && P.interacting && P.p2p_world <= 1 && !P.front_all && !KBE_NO_EARLY;
     if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     else pdl_enter();
     kbe_ctl* ctl = (kbe_ctl*)P.ctl;
@@ -1231,8 +1415,8 @@ __global__ void __launch_bounds__(32, KBE_COLL_MINB) collision_kernel(kbe_proble
     }
     const double delta = coll_delta(P, ctl, it);
     bool waited = !early;
-    if (coll_incremental(P, ctl, n, delta)) coll_body<true>(P, ctl, n, delta, waited);
-    else coll_body<false>(P, ctl, n, delta, waited);
+    if (coll_incremental(P, ctl, n, delta)) coll_body_incr(P, ctl, n, delta, waited);
+    else coll_body(P, ctl, n, delta, waited);
     if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -1729,8 +1913,14 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
 //   g(b) = sum_{bc <= b/TB} gc[bc][b]                                         (b < nf)
 // (+ the delta slots after an incremental evaluation); points 0..n-1, and n itself in
 // the corrector (the diagonal's I<(t_n, t_n)).
+#ifndef KBE_RED_BATCH
+#define KBE_RED_BATCH 6  // K3a loads in flight per thread
+#endif
+#ifndef KBE_RED_MINB
+#define KBE_RED_MINB 4  // K3a CTAs per SM (64 registers)
+#endif
 template <int INC>
-__global__ void __launch_bounds__(256, 4) reduce_kernel(kbe_problem P, int n, int phase, int it) {
+__global__ void __launch_bounds__(256, KBE_RED_MINB) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
@@ -1755,25 +1945,32 @@ __global__ void __launch_bounds__(256, 4) reduce_kernel(kbe_problem P, int n, in
         const int c0 = b / cts;
         const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
         const int na = nr + ns, ng = b < nf ? nr : 0;
-        constexpr int BATCH = 4;
-        cplx a = cz(), g = cz();
-        for (int i0 = 0; i0 < na; i0 += BATCH) {
-            cplx va[BATCH], vg[BATCH];
+        // I< row sums and I> column sums as two streams of independent loads (BATCH in
+        // flight, in-order adds): the sums are latency-bound, not byte-bound
+        auto sum = [&](auto batch_c, const cplx* lo, const cplx* hi, const cplx* lod, const cplx* hid, int cnt) {
+            constexpr int BATCH = decltype(batch_c)::value;
+            cplx acc = cz();
+            for (int i0 = 0; i0 < cnt; i0 += BATCH) {
+                cplx v[BATCH];
 #pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                const int q = i0 + u;
-                va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
-                vg[u] = q < ng ? gcP[q * cs] : cz();
-                if (INC && dl) {
-                    if (q < na) va[u] = cadd(va[u], q < nr ? rowD[q * cs] : colD[(c0 + q - nr) * cs]);
-                    if (q < ng) vg[u] = cadd(vg[u], gcD[q * cs]);
+                for (int u = 0; u < BATCH; ++u) {
+                    const int q = i0 + u;
+                    v[u] = q < cnt ? (q < nr ? lo[q * cs] : hi[(c0 + q - nr) * cs]) : cz();
+                    if (INC && lod && q < cnt) v[u] = cadd(v[u], q < nr ? lod[q * cs] : hid[(c0 + q - nr) * cs]);
                 }
-            }
 #pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                if (i0 + u < na) a = cadd(a, va[u]);
-                if (i0 + u < ng) g = cadd(g, vg[u]);
+                for (int u = 0; u < BATCH; ++u)
+                    if (i0 + u < cnt) acc = cadd(acc, v[u]);
             }
+            return acc;
+        };
+        cplx a, g;
+        if (INC && dl) {
+            a = sum(std::integral_constant<int, 4>{}, rowP, colP, rowD, colD, na);
+            g = sum(std::integral_constant<int, 4>{}, gcP, gcP, gcD, gcD, ng);
+        } else {
+            a = sum(std::integral_constant<int, KBE_RED_BATCH>{}, rowP, colP, nullptr, nullptr, na);
+            g = sum(std::integral_constant<int, KBE_RED_BATCH>{}, gcP, gcP, nullptr, nullptr, ng);
         }
         if (b < nf) a = cadd(a, ((const cplx*)P.fcol_part)[((int64_t)kl * N1 + b) * 4 + c]);
         ((cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c] = a;
@@ -2458,7 +2655,7 @@ static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
         else make_spec(s, sigma_frontier_kernel<2, 256>, grid, dim3(256), smem, *p, n, it, hb);
     }
 }
-static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
+static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it, bool after_sigma) {
     const int nkl = p->k_hi - p->k_lo;
     if (p->limit_mode) {
         const int T0 = n / TS + 1;
@@ -2469,7 +2666,8 @@ static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it) {
     }
     const int64_t total = (int64_t)coll_tiles(n, nkl) * (TS / coll_ts(n, nkl, 0));
     const int64_t cap = (int64_t)g_num_sms * g_coll_occ;
-    make_spec(s, collision_kernel, dim3((int)(total < cap ? total : cap)), dim3(32), sizeof(CollSmem), *p, n, it);
+    make_spec(s, collision_kernel, dim3((int)(total < cap ? total : cap)), dim3(32), sizeof(CollSmem), *p, n, it,
+              after_sigma ? 1 : 0);
 }
 // K3 split into K3a (reduce_kernel) + K3b for as-printed problems with many local k,
 // where the partial sums dominate K3 (KBE_SPLIT_MIN_K local k-points and up)
@@ -2537,7 +2735,7 @@ static void fill_spec(KSpec& s, const kbe_problem* p, const GNode& g, int n) {
     const int nn = g.it < 0 ? n - 1 : n, it = g.it < 0 ? 0 : g.it;
     switch (g.role) {
         case GR_SIGMA: spec_sigma(s, p, nn, it); break;
-        case GR_COLL: spec_collision(s, p, nn, it); break;
+        case GR_COLL: spec_collision(s, p, nn, it, true); break;
         case GR_HF: spec_hf(s, p, n, g.phase, it); break;
         case GR_UPD: spec_update(s, p, n, g.phase, it, g.next); break;
         default: spec_finish(s, p, n); break;
@@ -2743,15 +2941,18 @@ int kbe_sigma_slice(int32_t n_k, int32_t nb, const void* g_primary, const void* 
     return KBE_OK;
 }
 
-int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
+static int launch_collision(const kbe_problem* p, int n, int it, bool after_sigma, void* stream) {
     int rc = check_problem(p);
     if (rc) return rc;
     if (n < 0 || n > p->n_steps) { set_err("kbe_collision_frontier: n", cudaSuccess); return KBE_ERR_ARG; }
     if ((rc = ensure_attrs())) return rc;
     KSpec s;
-    spec_collision(s, p, n, it);
+    spec_collision(s, p, n, it, after_sigma);
     KBE_LAUNCH_SPEC(p->limit_mode ? "collision_langreth_kernel" : "collision_kernel", s);
     return KBE_OK;
+}
+int kbe_collision_frontier(const kbe_problem* p, int32_t n, int32_t it, void* stream) {
+    return launch_collision(p, n, it, false, stream);
 }
 
 int kbe_collision_slice(const kbe_problem* p, int32_t n, void* lesser_row, void* greater_row, void* lesser_col,
@@ -2835,13 +3036,13 @@ static int step_range(const kbe_problem* p, int n, int it0, int it1, void* strea
         // Algorithm 1 (propagator.py:328-382): Sigma(n-1), I(n-1), predictor, then
         // the corrector iterations [Sigma(n), I(n), corrector]; converged ones are no-ops.
         if (p->interacting && (rc = kbe_sigma_frontier(p, n - 1, 0, stream))) return rc;
-        if ((rc = kbe_collision_frontier(p, n - 1, 0, stream))) return rc;
+        if ((rc = launch_collision(p, n - 1, 0, p->interacting, stream))) return rc;
         if (p->hf && (rc = kbe_hf_mean(p, n, 0, 0, stream))) return rc;
         if ((rc = kbe_update(p, n, 0, 0, stream))) return rc;
     }
     for (int it = it0; it < it1; ++it) {
         if (p->interacting && (rc = kbe_sigma_frontier(p, n, it, stream))) return rc;
-        if ((rc = kbe_collision_frontier(p, n, it, stream))) return rc;
+        if ((rc = launch_collision(p, n, it, p->interacting, stream))) return rc;
         if (p->hf && (rc = kbe_hf_mean(p, n, 1, it, stream))) return rc;
         if ((rc = kbe_update(p, n, 1, it, stream))) return rc;
     }

@@ -320,13 +320,13 @@ class _PeerExchange:
 
 def _incremental_default(n_k: int) -> bool:
     """Incremental collision evaluations (collision_kernel): KBE_INCR=1/0 forces them on /
-    off; by default on for n_k >= 32, where K2 has enough tasks per launch to be closer
-    to HBM-bound and half-byte evaluations pay (profiles/r01/incr_ab_v18.jsonl: cfg3
-    +2.9 %, cfg5 +0 %, cfg2 -2.3 %)."""
+    off; by default on for n_k >= 8.  With their complex64 arithmetic they pay from
+    n_k = 16 up (profiles/r01/incr_ab_v23.jsonl: cfg2 +5.5 %, cfg3 +9 %, cfg5 +4.5 %);
+    at n_k = 2 the snapshot and shadow writes cost more than they save (cfg1 -8 %)."""
     env = os.environ.get("KBE_INCR")
     if env in ("0", "1"):
         return env == "1"
-    return n_k >= 32
+    return n_k >= 8
 
 
 def _dist_info(schedule: Schedule):

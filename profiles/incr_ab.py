@@ -1,6 +1,6 @@
 """Isolated K2 timing, full vs incremental evaluation, at one frontier.
 
-    python profiles/incr_ab.py [--workload cfg2] [--n 900] [--reps 20]
+    python profiles/incr_ab.py [--workload cfg2] [--n 900] [--reps 20] [--ncu full|incr]
 
 Propagates to step n-1, runs step n's predictor and first corrector, then times
 repeated corrector-1 collision launches at frontier n with the iteration-0 residual
@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--n", type=int, default=900)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--ncu", choices=["full", "incr"], default=None,
+                    help="bracket one launch of that mode with cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off); no timing")
     args = ap.parse_args()
     cfgw = bench.select_workload(args.workload)
     import paper_2505_19467_b200 as kb
@@ -61,6 +64,17 @@ def main():
         e1.record(st)
         torch.cuda.synchronize()
         return 1e3 * e0.elapsed_time(e1) / args.reps
+
+    if args.ncu:
+        res[0] = struct.unpack("<q", struct.pack("<d", 1e-3 if args.ncu == "full" else 2e-9))[0]
+        for _ in range(3):
+            _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        return
 
     nk = cfgw["n_k"]
     full_b = 64.0 * nk * ((n + 1) * (n + 2) + n * (n + 1))

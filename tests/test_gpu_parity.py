@@ -126,6 +126,37 @@ def test_collision_multi_tile_matches_oracle(kind, mode, n):
     assert rel_err(c.greater_col, want.greater_col) <= 1e-12
 
 
+def test_back_to_back_collision_launches_are_ordered():
+    """kbe_collision_frontier launched twice in a row (no Sigma launch between) must not
+    overlap the two grids (they share the task queue): the second evaluation equals a
+    lone one."""
+    from paper_2505_19467_b200 import _lib
+    from paper_2505_19467_b200._device import stream_ptr
+    from paper_2505_19467_b200.propagator import _Workspace
+    from paper_2505_19467_b200.state import pack_history
+
+    n_k, n = 4, 300
+    GL, GG, SL, SG = _random_sym_history(n_k, n, seed=5)
+    dev = torch.device("cuda:0")
+    ws = _Workspace.for_collision(n_k, n, 0.05, 0, pack_history(GL, GG, n, n).to(dev),
+                                  pack_history(SG, SL, n, n).to(dev), dev)
+    L, P, st = _lib.lib(), ws.problem_ptr(), stream_ptr()
+
+    def rows(seq):
+        for m in seq:
+            _lib.check(L.kbe_collision_frontier(P, m, 0, st))
+        out = [torch.empty((n_k, 2, 2, n + 1), dtype=torch.complex128, device=dev) for _ in range(2)]
+        out += [torch.empty((n_k, 2, 2, n), dtype=torch.complex128, device=dev) for _ in range(2)]
+        _lib.check(L.kbe_collision_slice(P, n, *[t.data_ptr() for t in out], st))
+        torch.cuda.synchronize()
+        return [t.cpu().numpy() for t in out]
+
+    lone = rows([n])
+    for _ in range(3):
+        for a, b in zip(rows([n - 1, n, n, n]), lone):
+            assert np.array_equal(a, b)
+
+
 def test_unknown_limit_mode_is_rejected():
     g = load_golden("collision.npz")
     with pytest.raises(kb.ConfigError):
