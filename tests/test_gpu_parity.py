@@ -145,16 +145,18 @@ def test_back_to_back_collision_launches_are_ordered():
     def rows(seq):
         for m in seq:
             _lib.check(L.kbe_collision_frontier(P, m, 0, st))
-        out = [torch.empty((n_k, 2, 2, n + 1), dtype=torch.complex128, device=dev) for _ in range(2)]
-        out += [torch.empty((n_k, 2, 2, n), dtype=torch.complex128, device=dev) for _ in range(2)]
-        _lib.check(L.kbe_collision_slice(P, n, *[t.data_ptr() for t in out], st))
+        f = seq[-1]
+        out = [torch.empty((n_k, 2, 2, f + 1), dtype=torch.complex128, device=dev) for _ in range(2)]
+        out += [torch.empty((n_k, 2, 2, f), dtype=torch.complex128, device=dev) for _ in range(2)]
+        _lib.check(L.kbe_collision_slice(P, f, *[t.data_ptr() for t in out], st))
         torch.cuda.synchronize()
         return [t.cpu().numpy() for t in out]
 
-    lone = rows([n])
-    for _ in range(3):
-        for a, b in zip(rows([n - 1, n, n, n]), lone):
-            assert np.array_equal(a, b)
+    for f in (n, n - 40):
+        lone = rows([f])
+        for _ in range(3):
+            for a, b in zip(rows([n, n - 40, n, f]), lone):
+                assert np.array_equal(a, b)
 
 
 def test_unknown_limit_mode_is_rejected():
