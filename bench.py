@@ -45,7 +45,7 @@ WORKLOADS = {
                  workload="cfg2: 1D Hubbard chain n_k=16, second-Born, 1000 time steps"),
     "cfg3": dict(n_k=64, n_steps=1000, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5, synth=True,
                  workload="cfg3: synthetic dense-interaction n_k=64 (seeded band/U tables), 1000 time steps"),
-    "cfg4": dict(n_k=32, n_steps=4000, dt=0.02, u=0.25, pulse_intensity=0.2, pulse_center=0.5,
+    "cfg4": dict(n_k=32, n_steps=4000, dt=0.02, u=0.2, pulse_intensity=0.2, pulse_center=0.5,
                  workload="cfg4: long-time n_k=32, 4000 time steps (history-streaming)"),
     "cfg5": dict(n_k=128, n_steps=500, dt=0.02, u=0.5, pulse_intensity=0.2, pulse_center=0.5,
                  workload="cfg5: large basis n_k=128, 500 time steps"),
