@@ -1267,6 +1267,10 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 for (int c = 0; c < 4; ++c) { Ab[c] = f32(csub(a[c], a0[c])); Bb[c] = f32(csub(l[c], l0[c])); }
             }
             __syncwarp();
+            // OFF: a block strictly below the diagonal (b < s for every lane and slice):
+            // no per-slice point tests
+            auto loop0 = [&](auto off_c) {
+            constexpr bool OFF = decltype(off_c)::value;
             for (int i = 0; i < mr; ++i, ++gcount) {
                 const int s = s0 + i;
                 const unsigned st = gcount % STG;
@@ -1279,9 +1283,9 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 fcx row[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) row[c] = make_float2(0.f, 0.f);
-                if (b <= s) {
+                if (OFF || b <= s) {
                     mm_acc(row, Ab, SU);
-                    if (b < s) {
+                    if (OFF || b < s) {
                         mm_bdag_acc(row, Bb, SL);
                         fcx As[4], Bs[4];
 #pragma unroll
@@ -1302,6 +1306,9 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
                 put(outD, s, (double)warp_rs8(v, lane));
             }
+            };
+            if (wb0 + TB <= s0) loop0(std::true_type{});
+            else loop0(std::false_type{});
             // history-part column sums -> the chunk's delta slot
             if (b <= s1) {
                 cplx* colD = (cplx*)P.col_delta + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
@@ -1354,6 +1361,13 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { X[c] = f32(csub(x[c], x0[c])); Y[c] = f32(csub(y[c], y0[c])); }
             }
+            // off-diagonal blocks: the weight w(j, b) (b < j) depends on j's parity only
+            // (trapezoid: not at all), so it is set once per task
+            const bool off = wb0 + TB <= s0;
+            const int je = (s0 + 1) & ~1;   // even and odd reference frontiers > b
+            const float w_even = (float)quad_w(je + 2, b, dt, P.quad), w_odd = (float)quad_w(je + 1, b, dt, P.quad);
+            auto loop1 = [&](auto off_c) {
+            constexpr bool OFF = decltype(off_c)::value;
             for (int i = 0; i < m; ++i, ++gcount) {
                 const int j = s0 + i;
                 const unsigned st = gcount % STG;
@@ -1366,10 +1380,10 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 fcx acc[4], t[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { acc[c] = make_float2(0.f, 0.f); t[c] = acc[c]; }
-                if (b <= j) {
-                    const float w = (float)quad_w(j, b, dt, P.quad);
+                if (OFF || b <= j) {
+                    const float w = OFF ? ((j & 1) ? w_odd : w_even) : (float)quad_w(j, b, dt, P.quad);
                     mm_bdag_acc(t, GL, X);             // GL X^dag
-                    if (b < j) {
+                    if (OFF || b < j) {
                         mm_adag_acc(acc, GU, Y);       // GU^dag Y
                     } else {
                         fcx u[4];
@@ -1387,6 +1401,9 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
                 put(outD, j, (double)warp_rs8(v, lane));
             }
+            };
+            if (off) loop1(std::true_type{});
+            else loop1(std::false_type{});
         }
     }
     coll_finish(ctl, n, delta, true);
