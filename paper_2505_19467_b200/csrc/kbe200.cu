@@ -769,7 +769,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // as-printed task height cap (slices per warp task; the per-slice vectors in shared
 // memory are sized by it) and the collision kernel's resident-CTA target
 #ifndef KBE_VEC_TS
-#define KBE_VEC_TS 16
+#define KBE_VEC_TS 32
 #endif
 #ifndef KBE_COLL_MINB
 #define KBE_COLL_MINB 16
@@ -778,7 +778,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define KBE_NO_EARLY 0   // 1: K2 always waits for K1 at entry (A/B switch)
 #endif
 #ifndef KBE_COLL_TASKS
-#define KBE_COLL_TASKS 16384
+#define KBE_COLL_TASKS 4096   // ~1.7 tasks per resident warp: taller tasks mean fewer
+                              // column partials for K3 (profiles/r01/task_size_v25.jsonl)
 #endif
 __host__ __device__ __forceinline__ int coll_tiles(int n, int nkl) {
     const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
