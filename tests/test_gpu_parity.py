@@ -334,6 +334,26 @@ def test_incremental_evaluations_match_full_evaluations(name, monkeypatch):
     assert float((a.sigma.hist - b.sigma.hist).abs().max()) <= 1e-13 * float(a.sigma.hist.abs().max())
 
 
+@pytest.mark.parametrize("quadrature", ["trapezoid", "simpson"])
+def test_incremental_evaluations_match_full_evaluations_long(quadrature, monkeypatch):
+    """The same over 300 steps at n_k = 8: the complex64 off-diagonal loops (blocks with
+    wb0 + 32 <= s0, per-task parity weights) and taller tasks run from n = 64 on."""
+    n_k, n_steps = 8, 300
+    model = kb.ModelConfig(u_protocol=0.5, pulse_intensity=0.2, pulse_center=0.5)
+    cfg = kb.StepConfig(dt=0.02, n_steps=n_steps, quadrature=quadrature, memory_budget=1 << 34)
+    runs = []
+    for incr in ("0", "1"):
+        monkeypatch.setenv("KBE_INCR", incr)
+        d = kb.PropagationDriver(kb.build_kgrid(n_k), model, cfg)
+        assert (d.ws.g_sh is not None) == (incr == "1")
+        runs.append((d, d.run()))
+    (a, ra), (b, rb) = runs
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    scale = float(a.state.hist.abs().max())
+    assert float((a.state.hist - b.state.hist).abs().max()) <= 1e-12 * scale
+    assert float((a.sigma.hist - b.sigma.hist).abs().max()) <= 1e-12 * float(a.sigma.hist.abs().max())
+
+
 @pytest.mark.parametrize("name", ["traj_nk16.npz", "traj_hf.npz", "traj_langreth.npz", "traj_dimer.npz"])
 def test_speculative_iteration_counts_equal_full_launches(name, monkeypatch):
     """run() launches only as many corrector iterations as earlier steps needed and
