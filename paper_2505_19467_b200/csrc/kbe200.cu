@@ -1864,7 +1864,7 @@ __device__ __forceinline__ void advance_col(const cplx* phi, const cplx* gprev, 
 // Points per CTA: up to 4 (and <= 512 threads), but small frontiers keep one point
 // per CTA so that the grid still spreads over the SMs.
 #ifndef KBE_UPD_BATCH
-#define KBE_UPD_BATCH 4   // partial loads in flight per operand and thread in K3
+#define KBE_UPD_BATCH 3   // partial loads in flight per operand and thread in K3 (4 spills; upd_batch_v25.jsonl)
 #endif
 static int g_upd_min_ctas = -1;   // KBE_UPD_MIN_CTAS (tuning knob)
 static int upd_ppc(int nkl, int n) {
