@@ -44,6 +44,7 @@ extern "C" {
 #define KBE_ERR_UNSUPPORTED 3
 
 #define KBE_MAX_ITER 16      /* StepConfig.max_iter ceiling on the device path */
+#define KBE_MAX_NK 128       /* largest n_k the Sigma kernel takes (kbe_max_n_k()) */
 #define KBE_MAX_RANKS 8      /* k-shard ranks of one NVLink/NVSwitch domain (peer-to-peer exchange) */
 #define KBE_TILE_B 32        /* collision warp-task: history points            */
 #define KBE_TILE_S 32        /* collision tile: time slices (a warp task takes 8, 16 or 32 of them) */
@@ -218,6 +219,11 @@ int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_g
 int kbe_run_iters(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t m, void* stream);
 int kbe_resume_step(const kbe_problem* p, int32_t n, int32_t m_done, void* stream);
 int64_t kbe_ctl_needs_more_offset(void);
+/* Byte offset of the hf_mode="on" k-sum of rho (4 complex) in the control block: the
+ * k-sharded host all-reduces exactly these bytes between kbe_hf_mean and kbe_build_phi. */
+int64_t kbe_ctl_hf_sum_offset(void);
+/* KBE_MAX_NK: the driver validates n_k against it before allocating anything. */
+int32_t kbe_max_n_k(void);
 
 /* Drop the step graph cached for this problem's control block (driver teardown). */
 int kbe_release(const kbe_problem* p);

@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("KBE_LIB") or os.environ.get("KBE200_LIB", os.path.joi
 
 KBE_OK, KBE_ERR_ARG, KBE_ERR_CUDA, KBE_ERR_UNSUPPORTED = 0, 1, 2, 3
 MAX_ITER = 16
+MAX_NK = 128       # KBE_MAX_NK: largest n_k of the Sigma kernel
 MAX_RANKS = 8
 TILE_B = 32
 TILE_S = 32
@@ -77,6 +78,8 @@ SIGNATURES = {
     "kbe_run_iters": (ctypes.c_int, [_p, _i32, _i32, _i32, _p]),
     "kbe_resume_step": (ctypes.c_int, [_p, _i32, _i32, _p]),
     "kbe_ctl_needs_more_offset": (_i64, []),
+    "kbe_ctl_hf_sum_offset": (_i64, []),
+    "kbe_max_n_k": (_i32, []),
     "kbe_p2p_bytes": (_i64, [_p, _i32]),
     "kbe_p2p_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(_p), _p]),
     "kbe_p2p_open": (ctypes.c_int, [_p, ctypes.POINTER(_p)]),

@@ -2636,8 +2636,9 @@ static int check_problem(const kbe_problem* p) {
         snprintf(g_err, sizeof(g_err), "limit_mode 'langreth' needs the langreth partial buffers");
         return KBE_ERR_ARG;
     }
-    if (p->n_k > 128) {
-        snprintf(g_err, sizeof(g_err), "n_k > 128 is not supported by the Sigma kernel (one stage-2 task per thread)");
+    if (p->n_k > KBE_MAX_NK) {
+        snprintf(g_err, sizeof(g_err), "n_k > %d is not supported by the Sigma kernel (one stage-2 task per thread)",
+                 KBE_MAX_NK);
         return KBE_ERR_UNSUPPORTED;
     }
     if (!p->phi) { set_err("kbe_problem.phi", cudaSuccess); return KBE_ERR_ARG; }
@@ -3110,6 +3111,8 @@ int kbe_resume_step(const kbe_problem* p, int32_t n, int32_t m_done, void* strea
 }
 
 int64_t kbe_ctl_needs_more_offset(void) { return (int64_t)offsetof(kbe_ctl, needs_more); }
+int64_t kbe_ctl_hf_sum_offset(void) { return (int64_t)offsetof(kbe_ctl, hf_sum); }
+int32_t kbe_max_n_k(void) { return KBE_MAX_NK; }
 
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream) {
     int rc = check_problem(p);

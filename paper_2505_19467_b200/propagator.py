@@ -351,6 +351,8 @@ class PropagationDriver:
         self.schedule.validate(grid.n_k)
         self.pool = pool
         quad, limit = validate_rule(step_cfg.quadrature, step_cfg.limit_mode)
+        if grid.n_k > _lib.MAX_NK:   # checked before any device allocation
+            raise ConfigError(f"n_k must be <= {_lib.MAX_NK} on the device path, got {grid.n_k}")
         if step_cfg.max_iter > _lib.MAX_ITER:
             raise ConfigError(f"max_iter must be <= {_lib.MAX_ITER} on the device path, got {step_cfg.max_iter}")
         capacity = max(step_cfg.n_steps, 1)
@@ -410,7 +412,7 @@ class PropagationDriver:
 
     def _allreduce_hf(self) -> None:
         import torch.distributed as dist
-        off = 208   # offsetof(kbe_ctl, hf_sum): 128 res + 64 nonfinite + 8 poisoned/pad, 16-aligned
+        off = int(_lib.lib().kbe_ctl_hf_sum_offset())   # offsetof(kbe_ctl, hf_sum) from the library
         all_reduce_device(self.ws.ctl[off: off + 64].view(torch.float64), dist.ReduceOp.SUM)
 
     # ------------------------------------------------------------------ speculative iteration counts

@@ -129,9 +129,11 @@ class Observables:
 
 
 def _ground_state(hist: torch.Tensor) -> None:
+    """Slice 0 in the packed layout: entry (plane c, point 0) is at slice_offset(0) + c*32."""
     hist.zero_()
-    hist[:, 0] = 1.0j          # G<(0,0)_00 = i   (state.py:85)
-    hist[:, 7 * 8] = -1.0j     # G>(0,0)_11 = -i  (state.py:86)
+    s0 = _lib.slice_offset(0)
+    hist[:, s0 + 0 * 32] = 1.0j     # plane 0 = G<(0,0)_00 = i   (state.py:85)
+    hist[:, s0 + 7 * 32] = -1.0j    # plane 7 = G>(0,0)_11 = -i  (state.py:86)
 
 
 def init_state(grid: KGrid, n_steps: int, dt: float, memory_budget: int = DEFAULT_MEMORY_BUDGET,

@@ -266,6 +266,96 @@ def cfg2_full_fixture():
           ref_seconds=np.array(time.time() - t0))
 
 
+def _synth_tables(n_k, n_steps, u):
+    """cfg3's synthetic system, the same draws as bench.model_kwargs:
+    eps_c = 1 + U(0,1), eps_v = -eps_c, U(t) = u (1 + 0.1 N(0,1)), default_rng(7)."""
+    rng = np.random.default_rng(7)
+    eps_c = 1.0 + rng.uniform(0.0, 1.0, n_k)
+    u_tab = u * (1.0 + 0.1 * rng.standard_normal(n_steps + 1))
+    return eps_c, u_tab
+
+
+# Long reference runs at the bench workloads' sizes.  name -> (file, n_k, N, model kwargs,
+# rows_k, rows_every).  U per workload as bench.WORKLOADS states it (DESIGN §6): cfg3's
+# tables at scale 0.75 (scale 1.0 diverges at step 868, 0.9 at step 987), cfg4 U = 0.2
+# (its 4000-step workload; 0.25 diverges at 3778), cfg5 U = 1.0 (finite for 500 steps).
+LONG_RUNS = {
+    "cfg3": ("traj_cfg3_full.npz", 64, 1000, "synth", 0.75),
+    "cfg4": ("traj_cfg4_prefix.npz", 32, 400, "plain", 0.2),
+    "cfg5": ("traj_cfg5_prefix.npz", 128, 120, "plain", 1.0),
+}
+
+
+def long_fixture(which):
+    """A bench workload run by the REAL reference, checkpointed: every
+    KBE_GOLDEN_SAVE_EVERY steps (default 50) the prefix computed so far is written,
+    so an interrupted run still leaves a usable golden.  Stores the per-step
+    observables, the equal-time diagonals, the final row G<(t_s, .) and column
+    G>(., t_s), and rows/columns of a few k every 100 steps."""
+    fname, n_k, N, kind, u = LONG_RUNS[which]
+    N = int(os.environ.get("KBE_GOLDEN_STEPS", N))
+    grid = kb.build_kgrid(n_k)
+    kw = dict(pulse_intensity=0.2, pulse_center=0.5)
+    if kind == "synth":
+        eps_c, u_tab = _synth_tables(n_k, LONG_RUNS[which][2], u)
+        kw.update(u_protocol=u_tab, eps_c_table=eps_c, eps_v_table=-eps_c)
+    else:
+        kw.update(u_protocol=u)
+    model = kb.ModelConfig(**kw)
+    cfg = kb.StepConfig(dt=0.02, n_steps=N, memory_budget=1 << 40)
+    workers = int(os.environ.get("KBE_GOLDEN_WORKERS", "6"))
+    shards = max(d for d in range(1, min(workers, n_k) + 1) if n_k % d == 0)
+    pool = kb.WorkerPool(workers)
+    every = int(os.environ.get("KBE_GOLDEN_SAVE_EVERY", "50"))
+    rows_k = np.arange(0, n_k, max(1, n_k // 4))
+    t0 = time.time()
+    drv = kb.PropagationDriver(grid, model, cfg, kb.Schedule(n_shards=shards, workers=workers), pool)
+    reps, rows, cols, row_steps = [], [], [], []
+    for n in range(1, N + 1):
+        reps.append(drv.step())
+        st = drv.state
+        if n % 100 == 0:
+            row_steps.append(n)
+            rows.append(st.lesser[rows_k, :, :, n, : n + 1].copy())
+            cols.append(st.greater[rows_k, :, :, : n + 1, n].copy())
+        if n % every == 0 or n == N:
+            idx = np.arange(n + 1)
+            out = dict(
+                n_k=np.array(n_k), n_steps=np.array(n), target_steps=np.array(LONG_RUNS[which][2]),
+                dt=np.array(0.02), u=np.array(u), pulse_intensity=np.array(0.2), pulse_center=np.array(0.5),
+                u_protocol=np.asarray(model.u_protocol, dtype=float),
+                iterations=np.array([r.iterations for r in reps]),
+                residual=np.array([r.residual for r in reps]),
+                drift=np.array([r.anticommutation_drift for r in reps]),
+                density=np.array([r.density for r in reps]),
+                diag_lesser=st.lesser[:, :, :, idx, idx],
+                diag_greater=st.greater[:, :, :, idx, idx],
+                final_row_lesser=st.lesser[:, :, :, n, : n + 1],
+                final_col_greater=st.greater[:, :, :, : n + 1, n],
+                rows_k=rows_k, row_steps=np.array(row_steps, dtype=int),
+                ref_seconds=np.array(time.time() - t0), workers=np.array(workers), shards=np.array(shards),
+            )
+            for s, r, c in zip(row_steps, rows, cols):
+                out[f"rows_lesser_{s}"] = r
+                out[f"cols_greater_{s}"] = c
+            if kind == "synth":
+                out["eps_c_table"] = np.asarray(model.eps_c_table)
+            _save(fname, **out)
+            print(f"  {which} step {n} {time.time() - t0:.0f}s", flush=True)
+
+
+def cfg3_fixture():
+    long_fixture("cfg3")
+
+
+def cfg4_fixture():
+    long_fixture("cfg4")
+
+
+def cfg5_fixture():
+    long_fixture("cfg5")
+
+
 def collision_row_fixture():
     """collision.collision_row (collision.py:141-162) on random inputs: vector and
     (T, P) matrix second-term weights, first-term weights shorter than T."""
