@@ -596,10 +596,9 @@ def run_ours(args):
     # each propagation adds kbe_init_history's 2 kernels.  Stream path: all max_iter
     # corrector iterations launch (converged ones as no-ops); graph path: only the
     # iterations that ran (the rest sit behind conditional nodes that stay off).
-    per_eval = 3 if drv.interactions_on else 2
-    # K3 split into reduce + update for as-printed problems with >= 32 local k (kbe200.cu)
-    if (drv.k_hi - drv.k_lo) >= 32 and drv.cfg.limit_mode == "as-printed" and not drv.use_graph:
-        per_eval += 1
+    per_eval = int(_lib.lib().kbe_launches_per_eval(drv.ws.problem_ptr()))
+    if drv.use_graph and world == 1:
+        per_eval = (3 if drv.interactions_on else 2) + int(drv.model.hf_mode == "on")   # graph: fused K3
     if world == 1 and drv.use_graph:
         per_prop = int(np.sum((1 + iters) * per_eval + 1)) + 2
     else:

@@ -222,6 +222,9 @@ int64_t kbe_ctl_needs_more_offset(void);
 /* Byte offset of the hf_mode="on" k-sum of rho (4 complex) in the control block: the
  * k-sharded host all-reduces exactly these bytes between kbe_hf_mean and kbe_build_phi. */
 int64_t kbe_ctl_hf_sum_offset(void);
+/* Kernels one evaluation launches on the stream path (Sigma, collision, [hf], [K3a],
+ * update): the launch count the bench reports.  -1 on an invalid problem. */
+int kbe_launches_per_eval(const kbe_problem* p);
 /* KBE_MAX_NK: the driver validates n_k against it before allocating anything. */
 int32_t kbe_max_n_k(void);
 

@@ -1924,21 +1924,24 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
     }
 }
 
-// K3a (split K3, as-printed with many local k): the fixed-order partial sums of K3's
-// phase A as a separate light kernel, one thread per (k, point, block entry), so that
-// the latency-bound sums run at full occupancy instead of under K3's register budget.
+// K3a (split K3, as-printed): the fixed-order partial sums of K3's phase A as a
+// separate streaming kernel, so the reduction runs at memory speed instead of as
+// ~n/16 dependent loads per thread under K3's register budget (round-1 K3: 22.8 us for
+// 47 MB at cfg2 n = 900, 18.7 % occupancy).
 //   a(b) = sum_{bc <= b/TB} row[bc][b] + sum_{b/ts <= sc <= nf/ts} col[sc][b] (+ fcol[b], b < nf)
 //   g(b) = sum_{bc <= b/TB} gc[bc][b]                                         (b < nf)
 // (+ the delta slots after an incremental evaluation); points 0..n-1, and n itself in
 // the corrector (the diagonal's I<(t_n, t_n)).
-#ifndef KBE_RED_BATCH
-#define KBE_RED_BATCH 6  // K3a loads in flight per thread
-#endif
-#ifndef KBE_RED_MINB
-#define KBE_RED_MINB 4  // K3a CTAs per SM (64 registers)
-#endif
+// One warp item = 2 points x 4 block entries of one local k (8 outputs, 128 contiguous
+// bytes per slot) x RED_G slot groups: lane g*8 + o sums the slots q = g, g + RED_G, ...
+// of the list [row slots, column slots] in order, RED_BATCH loads in flight; the groups
+// are combined by a fixed xor-shuffle tree.  The summation order depends only on
+// (n, b), so results are bitwise reproducible and independent of the launch shape.
+// Persistent grid, items strided over all warps.
+#define RED_G 4
+#define RED_BATCH 6
 template <int INC>
-__global__ void __launch_bounds__(256, KBE_RED_MINB) reduce_kernel(kbe_problem P, int n, int phase, int it) {
+__global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
@@ -1948,51 +1951,75 @@ __global__ void __launch_bounds__(256, KBE_RED_MINB) reduce_kernel(kbe_problem P
     const int npts = phase == 0 ? n : n + 1;
     const int cts = coll_ts(nf, nkl, 0);
     const bool dl = INC && ((const volatile kbe_ctl*)ctl)->incr_last;
-    const int64_t total = (int64_t)nkl * npts * 4;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(idx & 3), b = (int)((idx >> 2) % npts), kl = (int)((idx >> 2) / npts);
-        const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
-        const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
-        const cplx* rowP = (const cplx*)P.row_part + rb;
-        const cplx* colP = (const cplx*)P.col_part + cb;
-        const cplx* gcP = (const cplx*)P.gc_part + rb;
-        const cplx* rowD = dl ? (const cplx*)P.row_delta + rb : nullptr;
-        const cplx* colD = dl ? (const cplx*)P.col_delta + cb : nullptr;
-        const cplx* gcD = dl ? (const cplx*)P.gc_delta + rb : nullptr;
-        const int c0 = b / cts;
-        const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
-        const int na = nr + ns, ng = b < nf ? nr : 0;
-        // I< row sums and I> column sums as two streams of independent loads (BATCH in
-        // flight, in-order adds): the sums are latency-bound, not byte-bound
-        auto sum = [&](auto batch_c, const cplx* lo, const cplx* hi, const cplx* lod, const cplx* hid, int cnt) {
-            constexpr int BATCH = decltype(batch_c)::value;
-            cplx acc = cz();
-            for (int i0 = 0; i0 < cnt; i0 += BATCH) {
-                cplx v[BATCH];
+    const int lane = threadIdx.x & 31, g = lane >> 3, o = lane & 7;
+    const int pairs = (npts + 1) >> 1;
+    const int items = nkl * pairs;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += warps) {
+        const int kl = item / pairs;
+        const int b = (item % pairs) * 2 + (o >> 2), c = o & 3;
+        cplx a = cz(), gg = cz();
+        int na = 0, ng = 0;
+        if (b < npts) {
+            const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
+            const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
+            const cplx* rowP = (const cplx*)P.row_part + rb;
+            const cplx* colP = (const cplx*)P.col_part + cb;
+            const cplx* gcP = (const cplx*)P.gc_part + rb;
+            const cplx* rowD = (const cplx*)P.row_delta + rb;
+            const cplx* colD = (const cplx*)P.col_delta + cb;
+            const cplx* gcD = (const cplx*)P.gc_delta + rb;
+            const int c0 = b / cts;
+            const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
+            na = nr + ns;
+            ng = b < nf ? nr : 0;
+            // every load of a batch is issued unconditionally (address clamped to a valid
+            // slot, value masked afterwards): a branch around each load, or an add right
+            // after it, serialises the batch into one round trip per load
+            auto run = [&](auto with_delta) {
+                constexpr bool D = decltype(with_delta)::value;
+                constexpr int NB = D ? RED_BATCH / 2 : RED_BATCH;   // loads in flight: 4 * NB (D) or 2 * NB
+                for (int q0 = g; q0 < na || q0 < ng; q0 += NB * RED_G) {
+                    cplx va[NB], vg[NB], da[NB], dg[NB];
 #pragma unroll
-                for (int u = 0; u < BATCH; ++u) {
-                    const int q = i0 + u;
-                    v[u] = q < cnt ? (q < nr ? lo[q * cs] : hi[(c0 + q - nr) * cs]) : cz();
-                    if (INC && lod && q < cnt) v[u] = cadd(v[u], q < nr ? lod[q * cs] : hid[(c0 + q - nr) * cs]);
+                    for (int u = 0; u < NB; ++u) {
+                        const int q = q0 + u * RED_G;
+                        const bool rowq = q < nr || q >= na;   // past the list: row slot 0 (masked)
+                        const int64_t oa = q >= na ? 0 : (rowq ? (int64_t)q * cs : (int64_t)(c0 + q - nr) * cs);
+                        const int64_t ogg = q < ng ? (int64_t)q * cs : 0;
+                        va[u] = __ldcg((rowq ? rowP : colP) + oa);
+                        vg[u] = __ldcg(gcP + ogg);
+                        if (D) {
+                            da[u] = __ldcg((rowq ? rowD : colD) + oa);
+                            dg[u] = __ldcg(gcD + ogg);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < NB; ++u) {
+                        const int q = q0 + u * RED_G;
+                        if (D) { va[u] = cadd(va[u], da[u]); vg[u] = cadd(vg[u], dg[u]); }
+                        if (q < na) a = cadd(a, va[u]);
+                        if (q < ng) gg = cadd(gg, vg[u]);
+                    }
                 }
-#pragma unroll
-                for (int u = 0; u < BATCH; ++u)
-                    if (i0 + u < cnt) acc = cadd(acc, v[u]);
-            }
-            return acc;
-        };
-        cplx a, g;
-        if (INC && dl) {
-            a = sum(std::integral_constant<int, 4>{}, rowP, colP, rowD, colD, na);
-            g = sum(std::integral_constant<int, 4>{}, gcP, gcP, gcD, gcD, ng);
-        } else {
-            a = sum(std::integral_constant<int, KBE_RED_BATCH>{}, rowP, colP, nullptr, nullptr, na);
-            g = sum(std::integral_constant<int, KBE_RED_BATCH>{}, gcP, gcP, nullptr, nullptr, ng);
+            };
+            if (INC && dl) run(std::true_type{});
+            else run(std::false_type{});
         }
-        if (b < nf) a = cadd(a, ((const cplx*)P.fcol_part)[((int64_t)kl * N1 + b) * 4 + c]);
-        ((cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c] = a;
-        ((cplx*)P.g_red)[((int64_t)kl * N1 + b) * 4 + c] = g;
+        // groups (lanes o, o+8, o+16, o+24): ((g0 + g1) + (g2 + g3)); a + b == b + a exactly
+#pragma unroll
+        for (int off = 8; off < 32; off <<= 1) {
+            a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
+            a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
+            gg.x += __shfl_xor_sync(0xffffffffu, gg.x, off);
+            gg.y += __shfl_xor_sync(0xffffffffu, gg.y, off);
+        }
+        if (b < npts && g == 0) {
+            const int64_t oo = ((int64_t)kl * N1 + b) * 4 + c;
+            if (b < nf) a = cadd(a, __ldcg((const cplx*)P.fcol_part + oo));
+            ((cplx*)P.i_red)[oo] = a;
+            ((cplx*)P.g_red)[oo] = gg;
+        }
     }
 }
 
@@ -2019,8 +2046,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     const double dt = P.dt;
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     extern __shared__ cplx usm[];
-    cplx* sA = usm;                              // [PPC][nkl][4]  I<(t_nf, t_b)
-    cplx* sB = sA + PPC * nkl * 4;               // [PPC][nkl][4]  I>(t_b, t_nf)
+    cplx* sA = usm;                              // [nkl][PPC][4]  I<(t_nf, t_b)
+    cplx* sB = sA + PPC * nkl * 4;               // [nkl][PPC][4]  I>(t_b, t_nf)
     cplx* sC = sB + PPC * nkl * 4;               // [nkl][4]       I<(t_n, t_n)
     cplx* sRow = sC + nkl * 4;                   // [nkl][4]       new G<(n, n-1)
     cplx* sCol = sRow + nkl * 4;                 // [nkl][4]       new G>(n-1, n)
@@ -2073,8 +2100,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     if (RED) {
         // split K3: reduce_kernel (K3a) already summed the partials
         if (own) {
-            sA[(o * nkl + kl) * 4 + c] = ((const cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c];
-            sB[(o * nkl + kl) * 4 + c] = ((const cplx*)P.g_red)[((int64_t)kl * N1 + b) * 4 + c];
+            sA[(kl * PPC + o) * 4 + c] = ((const cplx*)P.i_red)[((int64_t)kl * N1 + b) * 4 + c];
+            sB[(kl * PPC + o) * 4 + c] = ((const cplx*)P.g_red)[((int64_t)kl * N1 + b) * 4 + c];
         }
         if (diag_cta && phase == 1)
             for (int i = tid; i < nkl * 4; i += T) sC[i] = ((const cplx*)P.i_red)[((int64_t)(i >> 2) * N1 + n) * 4 + (i & 3)];
@@ -2118,8 +2145,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         }
         if (!LANG && b < nf)   // the frontier slice's column-direction sums (own slot)
             a = cadd(a, ((const cplx*)P.fcol_part)[((int64_t)kl * N1 + b) * 4 + c]);
-        sA[(o * nkl + kl) * 4 + c] = a;
-        sB[(o * nkl + kl) * 4 + c] = g;
+        sA[(kl * PPC + o) * 4 + c] = a;
+        sB[(kl * PPC + o) * 4 + c] = g;
     }
     if (diag_cta && !RED) {
         if (LANG) {
@@ -2172,8 +2199,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
     double res = 0.0;
     bool fin = true;
     if (own) {
-        const cplx* A = sA + (o * nkl + kl) * 4;
-        const cplx* B = sB + (o * nkl + kl) * 4;
+        const cplx* A = sA + (kl * PPC + o) * 4;
+        const cplx* B = sB + (kl * PPC + o) * 4;
         // predictor column input: I>(t_b, t_{n-1}); b = n-1 takes greater_row[n-1]
         // (= -lesser_row as printed; the langreth reduction otherwise)
         auto IC0 = [&](int q) -> cplx {
@@ -2238,8 +2265,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 nu = ah(sandwich(gu, dj, dm), sandwich(gu, dm, dj));
             } else {
                 const int o1 = (n - 1) - b0;
-                const cplx* A1 = sA + (o1 * nkl + kl) * 4;
-                const cplx* B1 = sB + (o1 * nkl + kl) * 4;
+                const cplx* A1 = sA + (kl * PPC + o1) * 4;
+                const cplx* B1 = sB + (kl * PPC + o1) * 4;
                 const cplx* C = sC + kl * 4;
                 // src_l = mirror(row) - i dt (lesser_col[n-1] + lesser_row[n]) / 2
                 auto srcl = [&](int r, int q) -> cplx {
@@ -2688,18 +2715,24 @@ static void spec_collision(KSpec& s, const kbe_problem* p, int n, int it, bool a
     make_spec(s, collision_kernel, dim3((int)(total < cap ? total : cap)), dim3(32), sizeof(CollSmem), *p, n, it,
               after_sigma ? 1 : 0);
 }
-// K3 split into K3a (reduce_kernel) + K3b for as-printed problems with many local k,
-// where the partial sums dominate K3 (KBE_SPLIT_MIN_K local k-points and up)
+// K3 split into K3a (reduce_kernel) + K3b for as-printed problems with >= KBE_SPLIT_MIN_K
+// local k-points (env KBE_SPLIT_MIN_K overrides, for A/B runs): below that the fused
+// K3's partial sums are short and the extra launch costs more than it saves.
 #ifndef KBE_SPLIT_MIN_K
-#define KBE_SPLIT_MIN_K 32
+#define KBE_SPLIT_MIN_K 8
 #endif
+static int g_split_min_k = -1;
 static bool upd_split(const kbe_problem* p) {
-    return !p->limit_mode && p->i_red && p->g_red && (p->k_hi - p->k_lo) >= KBE_SPLIT_MIN_K;
+    if (g_split_min_k < 0) {
+        const char* e = getenv("KBE_SPLIT_MIN_K");
+        g_split_min_k = e ? atoi(e) : KBE_SPLIT_MIN_K;
+    }
+    return !p->limit_mode && p->i_red && p->g_red && (p->k_hi - p->k_lo) >= g_split_min_k;
 }
 static void spec_reduce(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
-    const int64_t total = (int64_t)(p->k_hi - p->k_lo) * (phase == 0 ? n : n + 1) * 4;
-    const int64_t cap = (int64_t)g_num_sms * 8;
-    const dim3 grid((unsigned)std::min<int64_t>((total + 255) / 256, cap));
+    const int64_t items = (int64_t)(p->k_hi - p->k_lo) * (((phase == 0 ? n : n + 1) + 1) / 2);
+    const int64_t cap = (int64_t)g_num_sms * 3;   // resident CTAs (__launch_bounds__(256, 3))
+    const dim3 grid((unsigned)std::min<int64_t>((items + 7) / 8, cap));
     if (p->g_sh) make_spec(s, reduce_kernel<1>, grid, dim3(256), 0, *p, n, phase, it);
     else make_spec(s, reduce_kernel<0>, grid, dim3(256), 0, *p, n, phase, it);
 }
@@ -3111,6 +3144,10 @@ int kbe_resume_step(const kbe_problem* p, int32_t n, int32_t m_done, void* strea
 }
 
 int64_t kbe_ctl_needs_more_offset(void) { return (int64_t)offsetof(kbe_ctl, needs_more); }
+int kbe_launches_per_eval(const kbe_problem* p) {
+    if (check_problem(p)) return -1;
+    return (p->interacting ? 1 : 0) + 1 + (p->hf ? 1 : 0) + (upd_split(p) ? 1 : 0) + 1;
+}
 int64_t kbe_ctl_hf_sum_offset(void) { return (int64_t)offsetof(kbe_ctl, hf_sum); }
 int32_t kbe_max_n_k(void) { return KBE_MAX_NK; }
 

@@ -440,8 +440,7 @@ class PropagationDriver:
         word = self.ws.ctl[off: off + 4].view(torch.int32)
         m = max(1, min(self.cfg.max_iter, getattr(self, "_spec_m", 2)))
         # kernels per evaluation (K1, K2, [hf], [K3a], K3) for the launch count the bench reports
-        per_eval = (int(self.interactions_on) + 2 + int(self.model.hf_mode == "on")
-                    + int((self.k_hi - self.k_lo) >= 32 and self.cfg.limit_mode == "as-printed"))
+        per_eval = int(L.kbe_launches_per_eval(P))
         self.spec_launches = 0
         pending = collections.deque()
         n = n0

@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--random", action="store_true",
                     help="fill the history with random values instead of propagating to n-1 (timing-only "
                          "library variants whose results are wrong)")
+    ap.add_argument("--ncu", action="store_true",
+                    help="after the set-up, run each step kernel once between cudaProfilerStart/Stop and exit "
+                         "(for ncu --profile-from-start off)")
     args = ap.parse_args()
     cfgw = bench.select_workload(args.workload)
     import paper_2505_19467_b200 as kb
@@ -58,6 +61,15 @@ def main():
     _lib.check(L.kbe_collision_frontier(P, n, 0, sp))
     _lib.check(L.kbe_update(P, n, 1, 0, sp))
     torch.cuda.synchronize()
+
+    if args.ncu:
+        torch.cuda.profiler.start()
+        _lib.check(L.kbe_sigma_frontier(P, n, 0, sp))
+        _lib.check(L.kbe_collision_frontier(P, n, 0, sp))
+        _lib.check(L.kbe_update(P, n, 1, 0, sp))
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
 
     def bench_fn(fn):
         for _ in range(3):

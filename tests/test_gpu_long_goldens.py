@@ -1,0 +1,105 @@
+"""Parity at the bench workloads' own sizes against long runs of the REAL reference
+(tests/golden/make_golden.py long_fixture): cfg3 (n_k = 64, 1000 steps, the
+north_star target), cfg4 (n_k = 32, 400-step prefix of the 4000-step workload) and
+cfg5 (n_k = 128, prefix of the 500-step workload).
+
+Each run goes through the production path (speculative iteration counts, the
+complex64 incremental collision corrections, the split K3 reduction, K1's
+sigma_frontier_kernel at n_k = 32 / 64 / 128) and once more with every evaluation in
+FP64 (KBE_INCR=0).  Tolerances: G< / G> rows, columns and equal-time diagonals
+<= 1e-10 relative to the largest reference entry (north_star); densities 1e-12
+absolute; iteration-count flips at the eps boundary are allowed (SURVEY finding 9)
+but bounded and reported.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_19467_b200 as kb  # noqa: E402
+from paper_2505_19467_b200.state import diagonal_blocks  # noqa: E402
+
+LONG = {"cfg3": "traj_cfg3_full.npz", "cfg4": "traj_cfg4_prefix.npz", "cfg5": "traj_cfg5_prefix.npz"}
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _load(name):
+    path = os.path.join(GOLDEN, LONG[name])
+    if not os.path.exists(path):
+        pytest.skip(f"{LONG[name]} not generated")
+    return np.load(path)
+
+
+def _model(g):
+    kw = dict(u_protocol=np.asarray(g["u_protocol"]) if "eps_c_table" in g else float(g["u"]),
+              pulse_intensity=float(g["pulse_intensity"]), pulse_center=float(g["pulse_center"]))
+    if "eps_c_table" in g:
+        kw.update(eps_c_table=np.asarray(g["eps_c_table"]), eps_v_table=-np.asarray(g["eps_c_table"]))
+    return kb.ModelConfig(**kw)
+
+
+def compare_long_golden(name):
+    """Run the golden's workload for its stored number of steps; return the error record."""
+    g = _load(name)
+    N = int(g["n_steps"])
+    drv = kb.PropagationDriver(kb.build_kgrid(int(g["n_k"])), _model(g),
+                               kb.StepConfig(dt=float(g["dt"]), n_steps=N, memory_budget=1 << 40))
+    reps = drv.run()
+    st = drv.state
+    sl = st.slice_view(N).cpu().numpy()                      # (k, 8, N+1)
+    err = {"workload": name, "steps": N, "incremental": drv.ws.g_sh is not None}
+    err["final_row_lesser"] = rel_err(sl[:, 0:4, :].reshape(-1, 2, 2, N + 1), g["final_row_lesser"])
+    err["final_col_greater"] = rel_err(sl[:, 4:8, :].reshape(-1, 2, 2, N + 1), g["final_col_greater"])
+    gl, gg = diagonal_blocks(st, 0, N)                        # (N+1, k, 2, 2)
+    err["diag_lesser"] = rel_err(np.moveaxis(gl, 0, -1), g["diag_lesser"])
+    err["diag_greater"] = rel_err(np.moveaxis(gg, 0, -1), g["diag_greater"])
+    ks = np.asarray(g["rows_k"])
+    worst = 0.0
+    for s in np.asarray(g["row_steps"]):
+        s = int(s)
+        v = st.slice_view(s).cpu().numpy()[ks]
+        worst = max(worst, rel_err(v[:, 0:4, :].reshape(-1, 2, 2, s + 1), g[f"rows_lesser_{s}"]),
+                    rel_err(v[:, 4:8, :].reshape(-1, 2, 2, s + 1), g[f"cols_greater_{s}"]))
+    err["rows_every_100"] = worst
+    err["density_abs"] = float(np.max(np.abs(np.array([r.density for r in reps]) - g["density"])))
+    err["drift_abs"] = float(np.max(np.abs(np.array([r.anticommutation_drift for r in reps]) - g["drift"])))
+    its = np.array([r.iterations for r in reps])
+    err["iteration_flips"] = int(np.sum(its != g["iterations"]))
+    err["iterations_hist"] = np.bincount(its).tolist()
+    drv.close()
+    return err
+
+
+def _check(err):
+    print(json.dumps(err))
+    for key in ("final_row_lesser", "final_col_greater", "diag_lesser", "diag_greater", "rows_every_100"):
+        assert err[key] <= 1e-10, (key, err)
+    assert err["density_abs"] <= 1e-12, err
+    assert err["drift_abs"] <= 1e-10, err
+    assert err["iteration_flips"] <= max(2, err["steps"] // 50), err
+
+
+@pytest.mark.parametrize("name", sorted(LONG))
+def test_long_reference_golden(name):
+    _check(compare_long_golden(name))
+
+
+@pytest.mark.parametrize("name", sorted(LONG))
+def test_long_reference_golden_fp64_only(name, monkeypatch):
+    monkeypatch.setenv("KBE_INCR", "0")
+    err = compare_long_golden(name)
+    assert not err["incremental"]
+    _check(err)
