@@ -49,12 +49,16 @@ extern "C" {
 #define KBE_TILE_B 32        /* collision warp-task: history points            */
 #define KBE_TILE_S 32        /* collision tile: time slices (a warp task takes 8, 16 or 32 of them) */
 #define KBE_COL_CHUNK 8      /* column-direction partial slots: one per 8 slices */
-#define KBE_REPORT_W 24      /* doubles per StepReport row (8 + KBE_MAX_ITER)  */
+#define KBE_REPORT_W 32      /* doubles per StepReport row (8 + KBE_MAX_ITER + 8) */
 
 /* Report row layout (doubles):
  *  0 step, 1 iterations, 2 residual, 3 converged, 4 anticommutation drift
  *  (max over local k), 5 sum over local k of n_v + n_c, 6 non-finite flag,
- *  7 reserved, 8.. residual history (KBE_MAX_ITER entries). */
+ *  7 sum over local k of Re Tr[h0(k; t_n) rho(k; t_n)] (one-body energy without the
+ *  hf term; rho = -i G<(t_n, t_n), h0 = build_h without hartree_fock, model.py:123-152),
+ *  8.. residual history (KBE_MAX_ITER entries), then sums over local k of rho_00,
+ *  rho_11, Re rho_01, Im rho_01 (the hf energy term needs the global k-mean of rho),
+ *  then 4 reserved. */
 
 /* Everything a step needs.  Scalars mirror StepConfig / ModelConfig
  * (propagator.py:44-52, model.py:27-37); pointers are caller-owned device
@@ -256,6 +260,13 @@ int kbe_p2p_publish(const kbe_problem* p, void* stream);
  * Entries beyond slice `frontier` are zero. */
 int kbe_unpack(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, int32_t frontier,
                int32_t which, void* out, void* stream);
+/* Retarded function of the packed G history in the reference layout:
+ * G^R(t,t') = theta(t-t') [G>(t,t') - G<(t,t')], theta(0) = theta0 on the diagonal
+ * (theta0 = 1: the t -> t'+ limit, G^R(t,t) = -i up to the anticommutation drift).
+ * A derived accessor (SURVEY finding 2: the reference has no G^R); its parity follows
+ * from G< / G> parity.  Entries with t < t' or beyond slice `frontier` are zero. */
+int kbe_unpack_retarded(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, int32_t frontier,
+                        double theta0, void* out, void* stream);
 /* Inverse: pack slices 0..frontier of a reference-layout pair (lower-stored,
  * upper-stored) into a packed history (zeroing nothing else). */
 int kbe_pack(const void* lower_full, const void* upper_full, int32_t k_local, int32_t n_steps,

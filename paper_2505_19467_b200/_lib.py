@@ -21,9 +21,9 @@ MAX_RANKS = 8
 TILE_B = 32
 TILE_S = 32
 COL_CHUNK = 8
-REPORT_W = 24
+REPORT_W = 32
 TAIL_CPLX = 16     # per-rank control tail of the all-gather chunk (KBE_TAIL_CPLX)
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 _p = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -90,6 +90,7 @@ SIGNATURES = {
     "kbe_p2p_read_u64": (ctypes.c_int, [_p, _p]),
     "kbe_unpack": (ctypes.c_int, [_p, _i64, _i32, _i32, _i32, _i32, _p, _p]),
     "kbe_pack": (ctypes.c_int, [_p, _p, _i32, _i32, _i32, _i64, _p, _p]),
+    "kbe_unpack_retarded": (ctypes.c_int, [_p, _i64, _i32, _i32, _i32, ctypes.c_double, _p, _p]),
 }
 
 _lib = None

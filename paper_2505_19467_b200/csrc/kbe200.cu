@@ -35,7 +35,7 @@
 #define KBE_COLL_EXP 0
 #endif
 
-#define KBE_ABI_VERSION 10
+#define KBE_ABI_VERSION 11
 
 typedef double2 cplx;
 
@@ -2414,6 +2414,13 @@ __global__ void finish_kernel(kbe_problem P, int n, int m_launched) {
     const int nloc = P.k_hi - P.k_lo;
     __shared__ double dens[256];
     __shared__ double drift[256];
+    __shared__ double en[256];
+    __shared__ double rho[256][4];
+    // one-body energy at the grid point t_n: h0(k; t_n) from the band tables, U(t_n) and the
+    // pulse amplitude at t_n (the step-n midpoint table: both round to grid point n,
+    // model.py:88-103), build_h (model.py:123-152) without the hf term, which the host adds
+    // from the k-sums of rho (it needs the global k-mean)
+    const double u_n = P.u_table[n], amp = P.amp[n];
     for (int kl = threadIdx.x; kl < nloc; kl += blockDim.x) {
         const cplx* c = (const cplx*)P.g_hist + (int64_t)kl * P.tri + slice_off(n);
         cplx gl[4], gu[4];
@@ -2424,12 +2431,33 @@ __global__ void finish_kernel(kbe_problem P, int n, int m_launched) {
             if (i == 0 || i == 3) t.y += 1.0;
             d = fmax(d, hypot(t.x, t.y));
         }
-        if (kl < 256) { dens[kl] = gl[0].y + gl[3].y; drift[kl] = d; }
+        // rho = -i G<(t_n, t_n) (propagator.py:272-273)
+        cplx r[4];
+        for (int i = 0; i < 4; ++i) r[i] = make_double2(gl[i].y, -gl[i].x);
+        const int k = P.k_lo + kl;
+        const cplx h01 = make_double2(amp * P.dipole_re, -amp * P.dipole_im);   // amp conj(d)
+        const cplx h10 = make_double2(amp * P.dipole_re, amp * P.dipole_im);    // amp d
+        // Re Tr[h0 rho] = h00 rho00 + h01 rho10 + h10 rho01 + h11 rho11
+        const double e = P.eps_v[k] * r[0].x + cmul(h01, r[2]).x + cmul(h10, r[1]).x + (P.eps_c[k] - u_n) * r[3].x;
+        if (kl < 256) {
+            dens[kl] = gl[0].y + gl[3].y;
+            drift[kl] = d;
+            en[kl] = e;
+            rho[kl][0] = r[0].x;
+            rho[kl][1] = r[3].x;
+            rho[kl][2] = r[1].x;
+            rho[kl][3] = r[1].y;
+        }
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    double ds = 0.0, dm = 0.0;
-    for (int kl = 0; kl < nloc && kl < 256; ++kl) { ds += dens[kl]; dm = fmax(dm, drift[kl]); }
+    double ds = 0.0, dm = 0.0, es = 0.0, rs[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kl = 0; kl < nloc && kl < 256; ++kl) {
+        ds += dens[kl];
+        dm = fmax(dm, drift[kl]);
+        es += en[kl];
+        for (int i = 0; i < 4; ++i) rs[i] += rho[kl][i];
+    }
     int iters = P.max_iter, conv = 0;
     for (int i = 0; i < m_launched; ++i)
         if (__longlong_as_double((long long)res_bits(P, ctl, i)) <= P.eps) { iters = i + 1; conv = 1; break; }
@@ -2446,9 +2474,10 @@ __global__ void finish_kernel(kbe_problem P, int n, int m_launched) {
     r[4] = dm;
     r[5] = ds;
     r[6] = nonfin;
-    r[7] = 0.0;
+    r[7] = es;
     for (int i = 0; i < KBE_MAX_ITER; ++i)
         r[8 + i] = i < iters ? __longlong_as_double((long long)res_bits(P, ctl, i)) : 0.0;
+    for (int i = 0; i < 4; ++i) r[8 + KBE_MAX_ITER + i] = rs[i];
     if (nonfin) ctl->poisoned = n;
 }
 
@@ -2513,6 +2542,31 @@ __global__ void unpack_kernel(const cplx* hist, int64_t tri, int kloc, int N, in
                 if (t <= tp) v = h[slice_off(tp) + sl_idx(4 + jm, t)];
                 else v = cneg(cconj(h[slice_off(t) + sl_idx(4 + m * 2 + j, tp)]));
             }
+        }
+        out[i] = v;
+    }
+}
+
+// G^R(t, t') = theta(t - t') [G>(t, t') - G<(t, t')] (SURVEY finding 2: a derived accessor,
+// the reference has none), theta(0) = theta0 on the equal-time diagonal; zero above the
+// diagonal and beyond slice `frontier`.  Reads both triangles of the packed G history.
+__global__ void unpack_retarded_kernel(const cplx* hist, int64_t tri, int kloc, int N, int frontier, double theta0,
+                                       cplx* out) {
+    const int64_t N1 = N + 1;
+    const int64_t total = (int64_t)kloc * 4 * N1 * N1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int tp = (int)(i % N1);
+        const int t = (int)((i / N1) % N1);
+        const int jm = (int)((i / (N1 * N1)) & 3);
+        const int kl = (int)(i / (N1 * N1 * 4));
+        const int j = jm >> 1, m = jm & 1;
+        const cplx* h = hist + kl * tri + slice_off(t);
+        cplx v = cz();
+        if (t <= frontier && tp <= t) {
+            const cplx gl = h[sl_idx(jm, tp)];                                   // G<(t, tp), lower-stored
+            const cplx gg = t == tp ? h[sl_idx(4 + jm, t)]                       // G>(t, t)
+                                    : cneg(cconj(h[sl_idx(4 + m * 2 + j, tp)]));  // -G>(tp, t)^dagger
+            v = cscale(csub(gg, gl), t == tp ? theta0 : 1.0);
         }
         out[i] = v;
     }
@@ -3192,6 +3246,21 @@ int kbe_unpack(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, 
     unpack_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const cplx*)hist, tri, k_local, n_steps, frontier,
                                                                  which, (cplx*)out);
     KBE_CHECK_LAUNCH("unpack_kernel");
+    return KBE_OK;
+}
+
+int kbe_unpack_retarded(const void* hist, int64_t tri, int32_t k_local, int32_t n_steps, int32_t frontier,
+                        double theta0, void* out, void* stream) {
+    if (!hist || !out || k_local < 1 || n_steps < 0 || frontier > n_steps) {
+        set_err("kbe_unpack_retarded", cudaSuccess);
+        return KBE_ERR_ARG;
+    }
+    const int64_t total = (int64_t)k_local * 4 * (n_steps + 1) * (int64_t)(n_steps + 1);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    unpack_retarded_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>((const cplx*)hist, tri, k_local, n_steps,
+                                                                          frontier, theta0, (cplx*)out);
+    KBE_CHECK_LAUNCH("unpack_retarded_kernel");
     return KBE_OK;
 }
 

@@ -71,6 +71,11 @@ class StepReport:
     density: float
     residual_history: list = field(default_factory=list)
     timings: dict = field(default_factory=dict)
+    # one-body energy (1/n_k) sum_k Tr[h(k; t_n) rho(k; t_n)] with h = build_h at the grid
+    # point t_n (model.py:123-152) and rho = -i G<(t_n, t_n) (propagator.py:272-273).  Not a
+    # reference field (the reference has no energy observable, SURVEY finding 2); appended
+    # with a default so the reference's positional fields are unchanged.
+    energy: float = 0.0
 
 
 def cayley_propagator(h: np.ndarray, dt: float) -> np.ndarray:
@@ -138,6 +143,9 @@ def combine_reports(stacked: np.ndarray) -> np.ndarray:
     out[:, 4] = stacked[:, :, 4].max(axis=0)
     out[:, 5] = stacked[:, :, 5].sum(axis=0)
     out[:, 6] = stacked[:, :, 6].max(axis=0)
+    out[:, 7] = stacked[:, :, 7].sum(axis=0)                       # energy k-sum
+    r0 = 8 + _lib.MAX_ITER
+    out[:, r0: r0 + 4] = stacked[:, :, r0: r0 + 4].sum(axis=0)     # rho k-sums
     return out
 
 
@@ -341,7 +349,7 @@ class PropagationDriver:
     """Owns the device state and Sigma history and advances them (propagator.py:229-392)."""
 
     def __init__(self, grid: KGrid, model: ModelConfig, step_cfg: StepConfig,
-                 schedule: Schedule | None = None, pool: WorkerPool | None = None):
+                 schedule: Schedule | None = None, pool: WorkerPool | None = None, timings: bool | None = None):
         model.validate()
         step_cfg.validate()
         self.grid = grid
@@ -393,6 +401,10 @@ class PropagationDriver:
         # conditional nodes).  Off by default: on B200 the conditional nodes cost more
         # than the no-op launches they remove (profiles/r01/launch_modes.jsonl).
         self.use_graph = 1 if os.environ.get("KBE_GRAPH", "0") == "1" else 0
+        # StepReport.timings (the reference's KernelTimers: sigma / collision / update,
+        # propagator.py:328-381) from CUDA events around every launch class.  Off by
+        # default: the events break the programmatic-launch overlap of the step kernels.
+        self.timings_enabled = (os.environ.get("KBE_TIMINGS", "0") == "1") if timings is None else bool(timings)
         if self.world > 1:
             self.publish_initial()
 
@@ -503,6 +515,59 @@ class PropagationDriver:
             self._gather_frontier()
         chk(L.kbe_finish_step(P, n, st), "kbe_finish_step")
 
+    def _launch_step_timed(self, n: int) -> list:
+        """The step's launches host-sequenced (kbe_step's order) with a CUDA event before
+        each class -- Sigma, collision, update ([hf] + [K3a] + K3) -- and after the last;
+        the finish kernel is timed into the last update.  Returns, per evaluation
+        ci = 0 (predictor, frontier n-1) .. max_iter, the event tuple."""
+        L, P, st = _lib.lib(), self.ws.problem_ptr(), stream_ptr()
+        stream = torch.cuda.current_stream()
+        chk = _lib.check
+
+        def ev():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+        out = []
+        calls = [(n - 1, 0, 0)] + [(n, 1, it) for it in range(self.cfg.max_iter)]
+        for ci, (nf, phase, it) in enumerate(calls):
+            e0 = ev()
+            if self.interactions_on:
+                chk(L.kbe_sigma_frontier(P, nf, it, st), "kbe_sigma_frontier")
+            e1 = ev()
+            chk(L.kbe_collision_frontier(P, nf, it, st), "kbe_collision_frontier")
+            e2 = ev()
+            if self.model.hf_mode == "on":
+                chk(L.kbe_hf_mean(P, n, phase, it, st), "kbe_hf_mean")
+                if self.world > 1:
+                    self._allreduce_hf()
+                    chk(L.kbe_build_phi(P, n, it, st), "kbe_build_phi")
+            chk(L.kbe_update(P, n, phase, it, st), "kbe_update")
+            if self.world > 1:
+                self._gather_frontier()
+            if ci == len(calls) - 1:
+                chk(L.kbe_finish_step(P, n, st), "kbe_finish_step")
+            out.append((e0, e1, e2, ev()))
+        return out
+
+    @staticmethod
+    def _fill_timings(reports: list, events: list) -> None:
+        """Seconds per class over the evaluations that did work (the predictor's and the
+        corrector iterations up to the step's count; later launches were no-ops)."""
+        torch.cuda.synchronize()
+        for rep, evs in zip(reports, events):
+            t = {"sigma": 0.0, "collision": 0.0, "update": 0.0}
+            for ci, (e0, e1, e2, e3) in enumerate(evs):
+                if ci > rep.iterations and ci < len(evs) - 1:
+                    continue
+                if ci <= rep.iterations:
+                    t["sigma"] += e0.elapsed_time(e1) * 1e-3
+                    t["collision"] += e1.elapsed_time(e2) * 1e-3
+                    t["update"] += e2.elapsed_time(e3) * 1e-3
+                else:   # the last (no-op) evaluation: only its finish kernel counts
+                    t["update"] += e2.elapsed_time(e3) * 1e-3
+            rep.timings = t
+
     # ------------------------------------------------------------------ reports
     def _reports(self, n0: int, n1: int) -> np.ndarray:
         rows = self.ws.reports[n0: n1 + 1].contiguous()
@@ -517,7 +582,23 @@ class PropagationDriver:
             step=int(row[0]), iterations=it, residual=float(row[2]), converged=bool(row[3]),
             anticommutation_drift=float(row[4]), density=float(row[5]) / self.grid.n_k,
             residual_history=[float(x) for x in row[8: 8 + it]], timings={},
+            energy=self._energy(row),
         )
+
+    def _energy(self, row: np.ndarray) -> float:
+        """Report row -> energy: the device's k-sum of Re Tr[h0 rho] plus, with
+        hf_mode="on", n_k Tr[hf m] for m the k-mean of rho (hartree_fock, model.py:106-120:
+        hf is the same for every k, so its energy only needs m)."""
+        nk = self.grid.n_k
+        e = float(row[7])
+        if self.model.hf_mode == "on":
+            r0 = 8 + _lib.MAX_ITER
+            m00, m11 = row[r0] / nk, row[r0 + 1] / nk
+            m01 = complex(row[r0 + 2], row[r0 + 3]) / nk
+            u = float(self.u_table[int(row[0])])
+            # Tr[hf m] = u m11 m00 - u m01 m10 - u m10 m01 + u m00 m11, m10 = conj(m01)
+            e += nk * float((u * m11 * m00 - u * m01 * np.conj(m01) - u * np.conj(m01) * m01 + u * m00 * m11).real)
+        return e / nk
 
     def _precheck(self, n: int) -> None:
         if n > self.capacity:
@@ -530,13 +611,18 @@ class PropagationDriver:
         """One time step (propagator.py:316-382); synchronises to return its report."""
         n = self.state.frontier + 1
         self._precheck(n)
-        self._launch_step(n)
+        events = [self._launch_step_timed(n)] if self.timings_enabled else None
+        if events is None:
+            self._launch_step(n)
         row = self._reports(n, n)[0]
         self.state.frontier = n
         if row[6] != 0.0:
             self._poisoned = n
             raise PoisonedStateError(f"non-finite values produced at step {n}")
-        return self._to_report(row)
+        rep = self._to_report(row)
+        if events is not None:
+            self._fill_timings([rep], events)
+        return rep
 
     def run(self, observer=None) -> list:
         """Advance n_steps steps (propagator.py:384-392).
@@ -558,7 +644,10 @@ class PropagationDriver:
             return []
         self._precheck(n0)
         n1 = min(last, self.capacity)
-        if self._speculative():
+        events = None
+        if self.timings_enabled:
+            events = [self._launch_step_timed(n) for n in range(n0, n1 + 1)]
+        elif self._speculative():
             self._run_speculative(n0, n1)
         elif self._device_sequenced():
             _lib.check(_lib.lib().kbe_run(self.ws.problem_ptr(), n0, n1, self.use_graph if self.world == 1 else 0,
@@ -579,6 +668,8 @@ class PropagationDriver:
                 self._poisoned = n
                 raise PoisonedStateError(f"non-finite values produced at step {n}")
             reports.append(self._to_report(row))
+        if events is not None:
+            self._fill_timings(reports, events)
         self.state.frontier = n1
         if last > self.capacity:
             raise CapacityError(f"step {self.capacity + 1} exceeds allocated capacity n_steps={self.capacity}")

@@ -93,13 +93,21 @@ class TwoTimeGF:
     def greater(self) -> np.ndarray:
         return to_host(self.greater_device())
 
-    def retarded(self) -> np.ndarray:
-        """Derived accessor G^R(t,t') = theta(t - t') [G>(t,t') - G<(t,t')] (SURVEY finding 2),
-        with theta(0) = 1/2 on the equal-time diagonal."""
-        diff = self.greater - self.lesser
+    def retarded_device(self, theta0: float = 1.0) -> torch.Tensor:
+        """G^R(t,t') = theta(t - t') [G>(t,t') - G<(t,t')] in the reference layout, on the
+        device (kbe_unpack_retarded), theta(0) = theta0 on the equal-time diagonal
+        (default 1: the t -> t'+ limit, G^R(t,t) = -i).  A derived accessor (SURVEY
+        finding 2: the reference has none); its parity follows from G< / G> parity."""
         n1 = self.n_steps + 1
-        theta = np.tril(np.ones((n1, n1)), -1) + 0.5 * np.eye(n1)
-        return diff * theta
+        out = torch.empty((self.n_k_local, 2, 2, n1, n1), dtype=torch.complex128, device=self.hist.device)
+        _lib.check(_lib.lib().kbe_unpack_retarded(self.hist.data_ptr(), self.hist.shape[1], self.n_k_local,
+                                                  self.n_steps, self.n_steps, float(theta0), out.data_ptr(),
+                                                  stream_ptr()), "kbe_unpack_retarded")
+        return out
+
+    def retarded(self, theta0: float = 1.0) -> np.ndarray:
+        """Host copy of retarded_device(theta0)."""
+        return to_host(self.retarded_device(theta0))
 
     # --- frontier slices (device, no host round trip) ----------------------------------
     def slice_view(self, s: int) -> torch.Tensor:

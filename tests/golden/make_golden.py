@@ -356,6 +356,43 @@ def cfg5_fixture():
     long_fixture("cfg5")
 
 
+def energy_fixture():
+    """One-body energy E(t_n) = (1/n_k) sum_k Re Tr[h(k; t_n) rho(k; t_n)] of the stored
+    reference trajectories, with the REFERENCE's own build_h (model.py:123-152, hf term
+    included) at every grid point and rho = -i G<(t_n, t_n) from the golden diagonals
+    (propagator.py:272-273).  The reference has no energy observable (SURVEY finding 2);
+    this pins the derived one to its Hamiltonian."""
+    out = {}
+    names = ["traj_dimer.npz", "traj_hf.npz", "traj_langreth.npz", "traj_nk64_synth.npz", "traj_simpson.npz",
+             "traj_nk4_full.npz", "traj_cfg2_full.npz"]
+    for name in names:
+        z = np.load(os.path.join(HERE, name))
+        n_k, N = int(z["n_k"]), int(z["n_steps"])
+        if "band_gap" in z:
+            kw = dict(band_gap=float(z["band_gap"]), hopping=float(z["hopping"]),
+                      u_protocol=(np.asarray(z["u_protocol"]) if np.asarray(z["u_protocol"]).ndim
+                                  else float(z["u_protocol"])),
+                      pulse_intensity=float(z["pulse_intensity"]), pulse_center=float(z["pulse_center"]),
+                      dipole=complex(z["dipole"]), hf_mode=str(z["hf_mode"]))
+            if "eps_c_table" in z:
+                kw.update(eps_c_table=np.asarray(z["eps_c_table"]), eps_v_table=np.asarray(z["eps_v_table"]))
+        else:   # traj_cfg2_full: model defaults + u, pulse
+            kw = dict(u_protocol=float(z["u"]), pulse_intensity=float(z["pulse_intensity"]),
+                      pulse_center=float(z["pulse_center"]))
+        model = kb.ModelConfig(**kw)
+        dt = float(z["dt"])
+        grid = kb.build_kgrid(n_k)
+        table = kb.u_values(model, N)
+        gl = np.asarray(z["diag_lesser"])                  # (n_k, 2, 2, N+1)
+        e = np.empty(N + 1)
+        for n in range(N + 1):
+            rho = -1j * gl[:, :, :, n]
+            h = kb.build_h(grid, model, n * dt, rho, dt, table)
+            e[n] = float(np.mean(np.einsum("kab,kba->k", h, rho).real))
+        out[name.replace(".npz", "")] = e
+    _save("energy.npz", **out)
+
+
 def collision_row_fixture():
     """collision.collision_row (collision.py:141-162) on random inputs: vector and
     (T, P) matrix second-term weights, first-term weights shorter than T."""

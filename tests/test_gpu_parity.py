@@ -372,3 +372,73 @@ def test_speculative_iteration_counts_equal_full_launches(name, monkeypatch):
     assert [r.residual_history for r in ra] == [r.residual_history for r in rb]
     assert [r.density for r in ra] == [r.density for r in rb]
     assert torch.equal(a.state.hist, b.state.hist) and torch.equal(a.sigma.hist, b.sigma.hist)
+
+
+# ------------------------------------------------------------------ derived observables
+ENERGY = ["traj_dimer", "traj_hf", "traj_langreth", "traj_nk64_synth", "traj_simpson", "traj_nk4_full"]
+
+
+@pytest.mark.parametrize("name", ENERGY)
+def test_energy_matches_reference_build_h(name):
+    """StepReport.energy (finish_kernel k-sums + the host hf term) against the energy of
+    the reference trajectory computed with the reference's own build_h
+    (tests/golden/energy.npz)."""
+    g = load_golden(name + ".npz")
+    e_ref = load_golden("energy.npz")[name]
+    reps = _driver_from_fixture(g).run()
+    e = np.array([r.energy for r in reps])
+    assert rel_err(e, e_ref[1:]) <= 1e-10
+
+
+def test_energy_of_cfg2_full_run():
+    import os
+    from conftest import GOLDEN
+    if not os.path.exists(os.path.join(GOLDEN, "traj_cfg2_full.npz")):
+        pytest.skip("traj_cfg2_full.npz not generated")
+    g = load_golden("traj_cfg2_full.npz")
+    model = kb.ModelConfig(u_protocol=float(g["u"]), pulse_intensity=float(g["pulse_intensity"]),
+                           pulse_center=float(g["pulse_center"]))
+    reps = kb.PropagationDriver(kb.build_kgrid(int(g["n_k"])), model,
+                                kb.StepConfig(dt=float(g["dt"]), n_steps=int(g["n_steps"]),
+                                              memory_budget=1 << 40)).run()
+    assert rel_err([r.energy for r in reps], load_golden("energy.npz")["traj_cfg2_full"][1:]) <= 1e-10
+
+
+@pytest.mark.parametrize("theta0", [1.0, 0.5])
+def test_retarded_accessor_on_device(theta0):
+    """G^R = theta(t - t') (G> - G<) from the device unpack equals the same formula on the
+    reference's full arrays (traj_nk4_full.npz) and has G^R(t,t) = -i theta0 up to the
+    anticommutation drift."""
+    g = load_golden("traj_nk4_full.npz")
+    drv = _driver_from_fixture(g)
+    reps = drv.run()
+    gr = drv.state.retarded(theta0)
+    n1 = int(g["n_steps"]) + 1
+    theta = np.tril(np.ones((n1, n1)), -1) + theta0 * np.eye(n1)
+    ref = (g["GG"] - g["GL"]) * theta
+    assert rel_err(gr, ref) <= 1e-10
+    # bitwise the same formula applied to the device's own unpacked arrays
+    np.testing.assert_array_equal(gr, (drv.state.greater - drv.state.lesser) * theta)
+    idx = np.arange(n1)
+    diag = gr[:, :, :, idx, idx]
+    drift = max(r.anticommutation_drift for r in reps)
+    assert np.abs(diag - (-1j * theta0) * np.eye(2)[None, :, :, None]).max() <= theta0 * drift + 1e-15
+
+
+def test_step_timings_from_cuda_events():
+    """StepReport.timings (sigma / collision / update seconds, the reference's KernelTimers)
+    are filled when enabled, and timing changes no result."""
+    g = load_golden("traj_nk16.npz")
+    plain = _driver_from_fixture(g).run()
+    drv = _driver_from_fixture(g)
+    drv.timings_enabled = True
+    timed = drv.run()
+    for a, b in zip(plain, timed):
+        assert a.density == b.density and a.iterations == b.iterations and a.residual == b.residual
+        assert set(b.timings) == {"sigma", "collision", "update"}
+        assert all(v > 0.0 for v in b.timings.values())
+    assert plain[0].timings == {}
+    one = _driver_from_fixture(g)
+    one.timings_enabled = True
+    rep = one.step()
+    assert rep.timings["collision"] > 0.0 and rep.density == plain[0].density

@@ -152,6 +152,7 @@ def test_cli_run_matches_reference_tables_and_trajectory(tmp_path):
     np.testing.assert_array_equal(ours[:, 0], ref[:, 0])
     assert np.sum(ours[:, 1] != ref[:, 1]) <= 1                                  # iteration counts
     np.testing.assert_allclose(ours[:, 4:6], ref[:, 4:6], rtol=0, atol=1e-10)    # drift, density
+    assert np.all(ours[:, 7] > 0) and np.all(ours[:, 8] > 0)                      # t_collision, t_update (events)
     # trajectory: same header bytes, values within the trajectory tolerance
     ob, rb = open(tmp_path / "t.kbe", "rb").read(), open(REF_KBE, "rb").read()
     assert ob[:24] == rb[:24] and len(ob) == len(rb)
