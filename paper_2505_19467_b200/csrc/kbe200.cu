@@ -14,7 +14,11 @@
 //   K4 finish_kernel           observables, finite check, StepReport row
 //   k-sharded ranks exchange the new frontier slice peer-to-peer from K3 (kbe_p2p_*).
 //
-// All arithmetic is FP64 / complex128.  There is no CPU fallback.
+// Arithmetic is FP64 / complex128, with one exception: a repeated collision evaluation
+// at the same frontier (incremental mode, n_k >= 8, KBE_INCR=0 disables it) computes its
+// correction M (v - v_full), a term <= 1e-7 of I, in complex64 from a complex64 shadow of
+// the history (relative error of I <= 2e-13 worst case, ~1e-14 typical); everything else,
+// including the slice-f terms of those evaluations, is FP64.  There is no CPU fallback.
 
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -877,7 +881,8 @@ __device__ __forceinline__ CollTask coll_task(int task, int nkl, int T0, int T1,
 // KBE_INCR_MAX_DELTA since that full one (the sum of the residuals the updates
 // measured in between) writes
 //   M (v - v_prev)   into delta slots, M streamed from a complex64 shadow of the history
-// (half the bytes; error |M| |dv| 2^-24 <= 6e-15 |I|, below a 50-ulp FP64 sum), and F(v)
+// (half the bytes; error ~2^-24 x (products + <= 32-term sums) x |M| |dv|: <= 2e-13 |I| worst
+// case, ~1e-14 typical), and F(v)
 // exactly in FP64.  K3 then sums base + delta per slot.  Slice f's column-direction sums
 // live in their own slot (fcol_part), so the chunk slots hold H only.  The shadow of
 // slice n-1 (G and Sigma) is written by the predictor update, once it is final.

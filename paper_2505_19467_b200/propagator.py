@@ -307,8 +307,27 @@ class _PeerExchange:
         cuda.synchronize()
         src = self.local + nbytes - 8
         _lib.check(_lib.lib().kbe_p2p_read_u64(src, _ct.c_void_p(word.data_ptr())), "kbe_p2p_read_u64")
-        if int(word[0]) != 0:
-            raise RuntimeError(f"peer-to-peer exchange timed out waiting for rank {int(word[0]) - 1}")
+        # share the watchdog words so that every rank raises together: a rank whose own
+        # wait did not time out would otherwise block in the next collective (_reports)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            words = [torch.zeros(1, dtype=torch.int64) for _ in range(dist.get_world_size())]
+            dist.all_gather(words, word) if dist.get_backend() == "gloo" else self._gather_words(words, word)
+            hit = [(r, int(w[0])) for r, w in enumerate(words) if int(w[0]) != 0]
+        else:
+            hit = [(self.rank, int(word[0]))] if int(word[0]) != 0 else []
+        if hit:
+            r, w = hit[0]
+            raise RuntimeError(f"peer-to-peer exchange timed out on rank {r} waiting for rank {w - 1}")
+
+    @staticmethod
+    def _gather_words(words, word):
+        """all_gather of the 8-byte watchdog words on a device backend (NCCL)."""
+        import torch.distributed as dist
+        dev = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in words]
+        dist.all_gather(dev, word.to("cuda"))
+        for w, d in zip(words, dev):
+            w.copy_(d.cpu())
 
     def close(self, free_local: bool = True) -> None:
         """Unmap the peers' buffers (after this rank's stream is idle).  The local buffer
