@@ -637,6 +637,196 @@ __global__ void __launch_bounds__(NT, 512 / NT) sigma_frontier_kernel(kbe_proble
     }
 }
 
+// ---- K1 in Fourier space (n_k a power of two) -----------------------------------------
+// With the DFT  x^(f) = sum_k x[k] w^{-fk}  (w = e^{2 pi i / n_k}) every stage of the
+// factorised Sigma above is a pointwise product (h = n_k/2 shifts give (-1)^f factors
+// that cancel pairwise):
+//   P^_jm(f)  = (-1)^f gp^_jm(f) gr^_mj(-f)              S1^_jm(f) = pref (-1)^f P^_{j'm'}(f) gp^_jm(f)
+//   X^_jm(f)  = gr^_{m'j'}(f) gp^_{j'm}(-f)              S2^_jm(f) = pref gp^_{jm'}(f) X^_jm(-f)
+// so
+//   Sigma^_jm(f) = pref gr^_{m'j'}(-f) [gp^_{j'm'}(f) gp^_jm(f) - gp^_{jm'}(f) gp^_{j'm}(f)]
+//                = pref s_jm det(gp^(f)) gr^_{m'j'}(-f),   s_jm = +1 (j = m), -1 (j != m)
+// (SURVEY probe P7: the FFT form equals sigma_slice to <= 7e-16).  Per pair b both
+// components use the same 8 vectors V1 = G<(t_b,t_n), V2 = G>(t_n,t_b) (comp 0: gp = V1,
+// gr = V2; comp 1 swapped), so one pair costs 8 forward and 8 inverse length-n_k FFTs,
+// O(n_k log n_k), instead of the 32 n_k^2 complex MACs of the correlations.  The kernel
+// is then bound by moving the G frontier slice in and the Sigma slice out.
+// One CTA = PB consecutive pairs (coalesced 16 B x PB runs per (k, plane)); shared
+// memory holds PB x 8 lines of n_k complex values (padded by TL per line so the TL
+// threads of one line and their neighbours' lines hit distinct banks).  Each line is
+// transformed by TL threads of one warp: radix-2 decimation in frequency (natural ->
+// bit-reversed order), the pointwise Sigma^ in bit-reversed order (f and -f handled by
+// one thread, in place), radix-2 decimation in time back to natural order.
+__host__ __device__ __forceinline__ bool sigma_fft_ok(int nk) { return nk >= 2 && nk <= KBE_MAX_NK && !(nk & (nk - 1)); }
+__host__ __device__ __forceinline__ int fft_tl(int nk, int pb) {
+    const int lines = pb * 8, t = SIGMA_THREADS / lines;
+    return t < 1 ? 1 : (t > nk / 2 ? nk / 2 : t);
+}
+// line stride: the TL threads of a line cover TL consecutive 16-byte slots; lines are
+// shifted so that each quarter-warp (8 slots) touches distinct banks
+__host__ __device__ __forceinline__ int fft_ls(int nk, int pb) {
+    const int tl = fft_tl(nk, pb);
+    return nk + (tl >= 8 ? 1 : tl);
+}
+static size_t sigma_fft_smem(int nk, int pb) {
+    // twiddles + lines + the two scaled determinants per (pair, frequency)
+    return ((size_t)pb * 8 * fft_ls(nk, pb) + nk + (size_t)pb * 2 * nk) * sizeof(cplx);
+}
+// pairs per CTA: at most one pointwise item (pair, frequency) per thread (PB n_k <= 256,
+// PB <= 32); the smallest PB whose grid still fits one wave of 3 CTAs per SM
+// (__launch_bounds__(256, 3)): a CTA's phases are latency-bound, so more CTAs in flight
+// help until a second, nearly empty wave would start
+static int sigma_fft_pb(int nk, int npairs, int sms) {
+    int pb = SIGMA_THREADS / nk;
+    pb = pb > 32 ? 32 : (pb < 1 ? 1 : pb);
+    while (pb > 1 && (npairs + pb / 2 - 1) / (pb / 2) <= 3 * sms) pb >>= 1;
+    return pb;
+}
+// DIF (forward, w^{-1}) or DIT (inverse, w^{+1}) radix-2 passes over one line of
+// NK = 2^LG points, TL = 2^LTL threads per line (consecutive lanes of one warp)
+template <int LG, bool INV>
+__device__ __forceinline__ void fft_line(cplx* d, const cplx* tw, int tl, int LTL, bool active) {
+    constexpr int NK = 1 << LG;
+#pragma unroll
+    for (int st = 0; st < LG; ++st) {
+        const int ls = INV ? st : LG - 1 - st;   // log2 of the butterfly span
+        const int s = 1 << ls;
+        if (active) {
+            for (int j = tl; j < NK / 2; j += 1 << LTL) {
+                const int r = j & (s - 1), a = ((j - r) << 1) + r, bb = a + s;
+                const cplx w = tw[r << (LG - 1 - ls)];
+                const cplx x = d[a];
+                if (!INV) {
+                    const cplx y = d[bb];
+                    d[a] = cadd(x, y);
+                    d[bb] = cmul(csub(x, y), w);
+                } else {
+                    const cplx y = cmul(d[bb], cconj(w));
+                    d[a] = cadd(x, y);
+                    d[bb] = csub(x, y);
+                }
+            }
+        }
+        __syncwarp();   // every lane takes part (a line's TL threads share one warp)
+    }
+}
+__host__ __device__ __forceinline__ int ilog2(int v) { int l = 0; while ((1 << (l + 1)) <= v) ++l; return l; }
+template <int LG>
+__global__ void __launch_bounds__(SIGMA_THREADS, 3) sigma_fft_kernel(kbe_problem P, int n, int it, int PB) {
+    pdl_enter();
+    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
+    if (kbe_skip(P, ctl, it)) return;
+    extern __shared__ cplx sm[];
+    constexpr int NK = 1 << LG;
+    const int LPB = ilog2(PB), TL = fft_tl(NK, PB), LTL = ilog2(TL), LS = fft_ls(NK, PB);
+    cplx* tw = sm;                        // w^{-j}, j < n_k
+    cplx* dat = sm + NK;                  // [PB * 8 lines][LS]
+    cplx* det = dat + PB * 8 * LS;        // [PB][2][n_k]: c det V1^(f), c det V2^(f)
+    const int b0 = blockIdx.x * PB, np = min(PB, n + 1 - b0);
+    const int nloc = P.k_hi - P.k_lo;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < NK; j += SIGMA_THREADS) {
+        double sn, cs;
+        sincospi(-2.0 * (double)j / (double)NK, &sn, &cs);
+        tw[j] = make_double2(cs, sn);
+    }
+    // gather: line p*8 + v holds V1_jm (v = jm) or V2_jm (v = 4 + jm) of pair b0 + p
+    //   V1 = G<(b,n) = -L(n,b)^dag (b < n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
+    // (p fastest: PB consecutive points of one plane are contiguous)
+    if (sharded(P)) {
+        // gathered buffer: rank chunks of [k_local][capacity slice] + control tail
+        const cplx* src = front_base(P);
+        const int64_t kstride = 8 * plane_len(P.n_steps), rstride = front_chunk(P);
+        for (int i = tid; i < (8 * NK) << LPB; i += SIGMA_THREADS) {
+            const int p = i & (PB - 1), c = (i >> LPB) & 7, k = i >> (LPB + 3);
+            if (p >= np) continue;
+            const int b = b0 + p, cc = c & 3;
+            const cplx v = __ldg(src + (k / nloc) * rstride + (k % nloc) * kstride + sl_idx(c, b));
+            const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
+            dat[(p * 8 + (c & 4) + jm) * LS + k] = b < n ? cneg(cconj(v)) : v;
+        }
+    } else {
+        const cplx* src = (const cplx*)P.g_hist + slice_off(n);
+        for (int i = tid; i < (8 * NK) << LPB; i += SIGMA_THREADS) {
+            const int p = i & (PB - 1), c = (i >> LPB) & 7, k = i >> (LPB + 3);
+            if (p >= np) continue;
+            const int b = b0 + p, cc = c & 3;
+            const cplx v = __ldg(src + k * P.tri + sl_idx(c, b));
+            const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
+            dat[(p * 8 + (c & 4) + jm) * LS + k] = b < n ? cneg(cconj(v)) : v;
+        }
+    }
+    __syncthreads();
+    const int line = tid >> LTL, tl = tid & (TL - 1);
+    const bool has_line = line < np * 8;
+    fft_line<LG, false>(dat + (has_line ? line : 0) * LS, tw, tl, LTL, has_line);
+    __syncthreads();
+    // pointwise Sigma^ in bit-reversed positions q (f = brev(q)), in place: comp 0 -> lines
+    // 0..3, comp 1 -> lines 4..7.  Threads walk q (conflict-free); the partner -f sits at
+    // brev(-f), whose low bits are the top bits of -f, so a quarter-warp's partner reads
+    // also hit distinct banks.
+    const double inv3 = 1.0 / ((double)NK * (double)NK * (double)NK);
+    const double un = P.u_table[n];
+    for (int i = tid; i < np * NK; i += SIGMA_THREADS) {
+        const int p = i >> LG, q = i & (NK - 1);
+        const cplx* L = dat + p * 8 * LS + q;
+        const double c = (P.u_table[b0 + p] * un) * inv3;
+        const cplx d1 = csub(cmul(L[0], L[3 * LS]), cmul(L[LS], L[2 * LS]));
+        const cplx d2 = csub(cmul(L[4 * LS], L[7 * LS]), cmul(L[5 * LS], L[6 * LS]));
+        det[(p * 2) * NK + q] = cscale(d1, c);
+        det[(p * 2 + 1) * NK + q] = cscale(d2, c);
+    }
+    __syncthreads();
+    {
+        constexpr int IT = 1;   // items per thread: np n_k <= 256 (sigma_fft_pb)
+        cplx m1[IT][4], m2[IT][4];
+#pragma unroll
+        for (int u = 0; u < IT; ++u) {
+            const int i = tid + u * SIGMA_THREADS;
+            if (i < np * NK) {
+                const int p = i >> LG, q = i & (NK - 1);
+                const int f = (int)(__brev((unsigned)q) >> (32 - LG));
+                const int g = (NK - f) & (NK - 1);
+                const int qg = (int)(__brev((unsigned)g) >> (32 - LG));
+                const cplx* L = dat + p * 8 * LS + qg;
+#pragma unroll
+                for (int v = 0; v < 4; ++v) { m1[u][v] = L[v * LS]; m2[u][v] = L[(4 + v) * LS]; }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < IT; ++u) {
+            const int i = tid + u * SIGMA_THREADS;
+            if (i < np * NK) {
+                const int p = i >> LG, q = i & (NK - 1);
+                cplx* L = dat + p * 8 * LS + q;
+                const cplx d1 = det[(p * 2) * NK + q], d2 = det[(p * 2 + 1) * NK + q];
+#pragma unroll
+                for (int jm = 0; jm < 4; ++jm) {
+                    const int o = jm == 0 ? 3 : (jm == 3 ? 0 : jm);   // (m'j') of (jm)
+                    cplx s0 = cmul(d1, m2[u][o]), s1 = cmul(d2, m1[u][o]);
+                    if (jm == 1 || jm == 2) { s0 = cneg(s0); s1 = cneg(s1); }
+                    L[jm * LS] = s0;
+                    L[(4 + jm) * LS] = s1;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    fft_line<LG, true>(dat + (has_line ? line : 0) * LS, tw, tl, LTL, has_line);
+    __syncthreads();
+    // comp 0 (lines 0..3) -> S<(t_b,t_n) = upper planes 4..7; comp 1 -> S>(t_n,t_b) = planes 0..3
+    cplx* dst = (cplx*)P.s_hist + slice_off(n);
+    for (int i = tid; i < (8 * nloc) << LPB; i += SIGMA_THREADS) {
+        const int p = i & (PB - 1), v = (i >> LPB) & 7, kl = i >> (LPB + 3);
+        if (p >= np) continue;
+        const int plane = v < 4 ? 4 + v : v - 4;
+        dst[(int64_t)kl * P.tri + sl_idx(plane, b0 + p)] = dat[(p * 8 + v) * LS + P.k_lo + kl];
+    }
+}
+#define KBE_FFT_LGS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7)
+
 // kernel-level sigma_slice API on batch-last (n_k,2,2,nb) buffers; one CTA per pair.
 __global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const cplx* gpi, const cplx* gri,
                                                           const double* u1, const double* u2, int k_lo,
@@ -2686,6 +2876,10 @@ static int ensure_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(sigma_frontier_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
+#define KBE_FFT_ATTR(L) if (e == cudaSuccess) e = cudaFuncSetAttribute(sigma_fft_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    KBE_FFT_LGS(KBE_FFT_ATTR)
+#undef KBE_FFT_ATTR
+    if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_fft)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmem));
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(collision)", e); return KBE_ERR_CUDA; }
     e = cudaFuncSetAttribute(collision_langreth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CollSmemL));
@@ -2743,7 +2937,22 @@ static int check_problem(const kbe_problem* p) {
 }
 
 // ---- launch specs of the step kernels (shared by the stream and graph paths)
+static int g_sigma_direct = -1;   // KBE_SIGMA_DIRECT=1: the O(n_k^2) correlation kernel (A/B)
 static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
+    if (g_sigma_direct < 0) {
+        const char* e = getenv("KBE_SIGMA_DIRECT");
+        g_sigma_direct = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (sigma_fft_ok(p->n_k) && !g_sigma_direct) {
+        const int pb = sigma_fft_pb(p->n_k, n + 1, g_num_sms);
+        const dim3 grid((n + 1 + pb - 1) / pb), block(SIGMA_THREADS);
+        const size_t smem = sigma_fft_smem(p->n_k, pb);
+        switch (ilog2(p->n_k)) {
+#define KBE_FFT_CASE(L) case L: make_spec(s, sigma_fft_kernel<L>, grid, block, smem, *p, n, it, pb); return;
+            KBE_FFT_LGS(KBE_FFT_CASE)
+#undef KBE_FFT_CASE
+        }
+    }
     const int hb = sigma_hb_launch(p->n_k, 2 * (n + 1), g_num_sms);
     const dim3 grid((2 * (n + 1) + hb - 1) / hb);
     const size_t smem = (size_t)hb * SgDims(p->n_k).per * sizeof(cplx);

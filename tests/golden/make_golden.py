@@ -26,7 +26,11 @@ from kbesolve.state import mirror_frontier  # noqa: E402
 
 
 def _save(name, **arrays):
-    path = os.path.join(HERE, name)
+    # KBE_GOLDEN_OUT: write somewhere else (a long checkpointed run must not overwrite
+    # a longer committed prefix with its first checkpoints)
+    out_dir = os.environ.get("KBE_GOLDEN_OUT", HERE)
+    os.makedirs(out_dir, exist_ok=True)
+    path = os.path.join(out_dir, name)
     np.savez_compressed(path, **arrays)
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)")
 
