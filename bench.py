@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -405,10 +406,11 @@ def _reset(kb, drv):
         drv.publish_initial()
 
 
-def _k1_peak():
-    """FP64 roofline denominator for K1: MEASURED_PEAKS.json has no FP64 entry, so the
-    DFMA peak measured on a B200 of this pool (profiles/fp64_peak.cu ->
-    profiles/r01/fp64_peak.json), else the datasheet FP64 figure."""
+def _k1_peak(kind="dfma"):
+    """FP64 roofline denominators for K1: MEASURED_PEAKS.json has no FP64 entry, so the
+    DFMA / DMMA peaks measured on a B200 of this pool (profiles/fp64_peak.cu ->
+    profiles/r01/fp64_peak.json, profiles/dmma_peak.cu -> profiles/r02/dmma_peak.jsonl),
+    else the datasheet FP64 figure."""
     try:
         p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         if "fp64_tflops" in p:
@@ -416,10 +418,41 @@ def _k1_peak():
     except Exception:
         pass
     try:
+        if kind == "dmma":
+            for line in open(os.path.join(ROOT, "profiles", "r02", "dmma_peak.jsonl")):
+                d = json.loads(line)
+                if "dmma_tflops" in d:
+                    return float(d["dmma_tflops"]) * 1e3, "measured DMMA m8n8k4 peak (profiles/r02/dmma_peak.jsonl)"
         p = json.load(open(os.path.join(ROOT, "profiles", "r01", "fp64_peak.json")))
         return float(p["fp64_tflops"]) * 1e3, "measured DFMA peak (profiles/r01/fp64_peak.json)"
     except Exception:
         return 37000.0, "datasheet (HGX B200 FP64 / FP64 tensor)"
+
+
+def _sigma_variant(n_k):
+    """The K1 kernel a launch uses (propagator._sigma_variant_from_env / spec_sigma)."""
+    env = os.environ.get("KBE_SIGMA", "auto")
+    if env == "auto":
+        return "fft" if n_k >= 2 and not (n_k & (n_k - 1)) else "dft"
+    return env
+
+
+def _k1_work(variant, nkg, nkl, pairs):
+    """(executed flops, HBM bytes) of one K1 launch over `pairs` pairs.  Bytes: the G
+    frontier slice (all k) in and the Sigma slice (local k) out, 8 planes of c128 each.
+    Flops: fft = 16 length-n_k transforms per pair (radix-2 count 5 N log2 N + 6 N for the
+    four-step twiddles) + the pointwise det / product (70 N); dft = 4 real DMMA MACs per
+    complex MAC of the forward (8 n_k^2) and inverse (8 n_k n_k_local) GEMMs; direct = the
+    four correlations (128 n_k^2 per pair and component)."""
+    byt = pairs * 8 * 16.0 * (nkg + nkl)
+    if variant == "fft":
+        lg = math.log2(nkg)
+        fl = pairs * (16 * (5 * nkg * lg + 6 * nkg) + 70 * nkg)
+    elif variant == "dft":
+        fl = pairs * 2 * 4 * (8 * nkg * nkg + 8 * nkg * nkl)
+    else:
+        fl = pairs * 2 * 128.0 * nkg * nkg
+    return fl, byt
 
 
 def _collision_roofline(kb, drv, hbm_peak):
@@ -475,9 +508,10 @@ def _collision_roofline(kb, drv, hbm_peak):
     prev_f = full_f = -1
     dsum = 0.0
     tot_b, tot_t, launches, n_incr = 0.0, 0.0, 0, 0
-    k1_f, k1_t, k1_n, k1_fdir = 0.0, 0.0, 0, 0.0
+    k1_f, k1_t, k1_n, k1_fdir, k1_b = 0.0, 0.0, 0, 0.0, 0.0
     k3_t, k3_late = 0.0, []
     nkg = drv.grid.n_k
+    variant = _sigma_variant(nkg)
     for n, ci, nf, e0, e1, s0, u1 in ev:
         if ci > iters[n - 1]:
             continue    # converged: launch was a no-op
@@ -499,9 +533,9 @@ def _collision_roofline(kb, drv, hbm_peak):
         tot_t += e0.elapsed_time(e1) * 1e-3
         launches += 1
         if drv.interactions_on:
-            # factorised Sigma (executed): P, Sigma1 and the two Sigma2 correlations,
-            # 32 n_k^2 flop each per pair and component, both components, n+1 pairs
-            k1_f += 2.0 * (nf + 1) * 128.0 * nkg * nkg
+            fl, byt = _k1_work(variant, nkg, nk, nf + 1)
+            k1_f += fl
+            k1_b += byt
             k1_fdir += 2.0 * (nf + 1) * (56.0 * nkg ** 3 + 64.0 * nkg ** 2)
             k1_t += s0.elapsed_time(e0) * 1e-3
             k1_n += 1
@@ -513,15 +547,24 @@ def _collision_roofline(kb, drv, hbm_peak):
     achieved = tot_b / tot_t / 1e9
     k1 = None
     if k1_n:
-        pk, pk_kind = _k1_peak()
+        pk, pk_kind = _k1_peak("dmma" if variant == "dft" else "dfma")
         a1 = k1_f / k1_t / 1e9
-        k1 = {"bound": "fp64", "achieved": a1, "peak": pk, "unit": "GFLOP/s", "frac": a1 / pk, "peak_kind": pk_kind,
-              "kernel": "sigma_frontier_kernel (K1)", "launches_with_work": k1_n, "kernel_seconds": k1_t,
-              "share_of_propagation": k1_t / step_s,
-              "flops_per_launch_formula": "2*(n+1)*128*n_k^2 (factorised Sigma, executed)",
+        names = {"fft": "sigma_fft_kernel (K1, four-step FFTs)", "dft": "sigma_dft_kernel (K1, DMMA DFT GEMMs)",
+                 "direct": "sigma_frontier_kernel (K1, O(n_k^2) correlations)"}
+        k1 = {"variant": variant, "kernel": names.get(variant, variant),
+              "bound": {"fft": "latency", "dft": "fp64 tensor (DMMA)", "direct": "fp64"}.get(variant, "fp64"),
+              "achieved": a1, "peak": pk, "unit": "GFLOP/s", "frac": a1 / pk, "peak_kind": pk_kind,
+              "hbm_gbs": k1_b / k1_t / 1e9, "hbm_frac": k1_b / k1_t / 1e9 / hbm_peak,
+              "launches_with_work": k1_n, "kernel_seconds": k1_t, "share_of_propagation": k1_t / step_s,
+              "us_per_launch": k1_t / k1_n * 1e6,
+              "flops_per_launch_formula": {
+                  "fft": "(n+1)[16(5 n_k log2 n_k + 6 n_k) + 70 n_k] (FFTs + pointwise, executed)",
+                  "dft": "(n+1) 8 (8 n_k^2 + 8 n_k n_k_local) (real DMMA flops, executed)",
+                  "direct": "2(n+1) 128 n_k^2 (factorised correlations, executed)"}.get(variant),
+              "bytes_per_launch_formula": "(n+1) 8 planes 16 B (n_k + n_k_local)",
               "reference_algorithm_gflops": k1_fdir / k1_t / 1e9,
-              "reference_algorithm_note": "direct Alg. 2 count 2(n+1)(56 n_k^3 + 64 n_k^2) over the same time; "
-                                          "exceeds the FP64 peak because the factorised form does ~n_k/2 fewer flops"}
+              "reference_algorithm_note": "direct Alg. 2 count 2(n+1)(56 n_k^3 + 64 n_k^2) over the same time: the "
+                                          "rate the reference's own algorithm would need to match this kernel"}
     return {
         "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
         "traffic": None, "kernel": "collision_kernel (K2)", "launches_with_work": launches,

@@ -229,6 +229,12 @@ int64_t kbe_ctl_hf_sum_offset(void);
 /* Kernels one evaluation launches on the stream path (Sigma, collision, [hf], [K3a],
  * update): the launch count the bench reports.  -1 on an invalid problem. */
 int kbe_launches_per_eval(const kbe_problem* p);
+/* Sigma kernel variant for every later K1 launch of this process (env KBE_SIGMA, read
+ * by the driver): 0 auto (FFT for power-of-two n_k, DMMA DFT GEMMs otherwise), 1 FFT,
+ * 2 DMMA DFT GEMMs, 3 the O(n_k^2) correlation kernel.  Returns the previous setting,
+ * -1 for an unknown kind.  Replaces nothing in the reference: its sigma_second
+ * (selfenergy.py:139-203) has one algorithm; this selects how K1 computes the same Sigma. */
+int kbe_set_sigma_variant(int32_t kind);
 /* KBE_MAX_NK: the driver validates n_k against it before allocating anything. */
 int32_t kbe_max_n_k(void);
 

@@ -80,6 +80,7 @@ SIGNATURES = {
     "kbe_ctl_needs_more_offset": (_i64, []),
     "kbe_ctl_hf_sum_offset": (_i64, []),
     "kbe_max_n_k": (_i32, []),
+    "kbe_set_sigma_variant": (ctypes.c_int, [_i32]),
     "kbe_launches_per_eval": (ctypes.c_int, [_p]),
     "kbe_p2p_bytes": (_i64, [_p, _i32]),
     "kbe_p2p_alloc": (ctypes.c_int, [_i64, ctypes.POINTER(_p), _p]),

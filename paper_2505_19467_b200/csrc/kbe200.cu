@@ -652,74 +652,141 @@ __global__ void __launch_bounds__(NT, 512 / NT) sigma_frontier_kernel(kbe_proble
 // O(n_k log n_k), instead of the 32 n_k^2 complex MACs of the correlations.  The kernel
 // is then bound by moving the G frontier slice in and the Sigma slice out.
 // One CTA = PB consecutive pairs (coalesced 16 B x PB runs per (k, plane)); shared
-// memory holds PB x 8 lines of n_k complex values (padded by TL per line so the TL
-// threads of one line and their neighbours' lines hit distinct banks).  Each line is
-// transformed by TL threads of one warp: radix-2 decimation in frequency (natural ->
-// bit-reversed order), the pointwise Sigma^ in bit-reversed order (f and -f handled by
-// one thread, in place), radix-2 decimation in time back to natural order.
+// memory holds PB x 8 lines of n_k complex values.  Each length-n_k transform is a
+// four-step FFT, n_k = R1 R2 (R1 = 2^ceil(LG/2), R2 = 2^floor(LG/2)), n = R2 n1 + n2,
+// f = f1 + R1 f2:
+//   pass 1 (one thread per (line, n2)): R1-point DFT over n1 in registers, times
+//          w^{-f1 n2}, written back in place (position R2 f1 + n2);
+//   pass 2 (one thread per (line, f1)): R2-point DFT over n2 in registers, written to
+//          the natural position f1 + R1 f2.
+// Two shared-memory round trips per transform instead of log2(n_k) radix-2 stages; the
+// input and output are in natural order, so the pointwise phase pairs f with n_k - f
+// directly.  Lines are padded by one slot per R2 (pad()) so that pass 2's stride-R2 reads
+// hit distinct banks.
 __host__ __device__ __forceinline__ bool sigma_fft_ok(int nk) { return nk >= 2 && nk <= KBE_MAX_NK && !(nk & (nk - 1)); }
-__host__ __device__ __forceinline__ int fft_tl(int nk, int pb) {
-    const int lines = pb * 8, t = SIGMA_THREADS / lines;
-    return t < 1 ? 1 : (t > nk / 2 ? nk / 2 : t);
-}
-// line stride: the TL threads of a line cover TL consecutive 16-byte slots; lines are
-// shifted so that each quarter-warp (8 slots) touches distinct banks
-__host__ __device__ __forceinline__ int fft_ls(int nk, int pb) {
-    const int tl = fft_tl(nk, pb);
-    return nk + (tl >= 8 ? 1 : tl);
+__host__ __device__ constexpr int fft_r1(int lg) { return 1 << ((lg + 1) / 2); }
+__host__ __device__ constexpr int fft_r2(int lg) { return 1 << (lg / 2); }
+__host__ __device__ __forceinline__ int fft_pad(int i, int lg) { return fft_r2(lg) >= 4 ? i + (i >> (lg / 2)) : i; }
+// line stride: >= the padded length, = R2 mod 8 when a quarter-warp spans several lines
+// in pass 1 (R2 threads per line), so their slots fall in distinct banks
+__host__ __device__ __forceinline__ int fft_ls(int lg) {
+    const int len = fft_pad((1 << lg) - 1, lg) + 1, r2 = fft_r2(lg);
+    return ((len + 7) & ~7) + (r2 < 8 ? r2 : 1);
 }
 static size_t sigma_fft_smem(int nk, int pb) {
     // twiddles + lines + the two scaled determinants per (pair, frequency)
-    return ((size_t)pb * 8 * fft_ls(nk, pb) + nk + (size_t)pb * 2 * nk) * sizeof(cplx);
+    int lg = 0;
+    while ((1 << lg) < nk) ++lg;
+    return ((size_t)pb * 8 * fft_ls(lg) + nk + (size_t)pb * 2 * nk) * sizeof(cplx);
 }
 // pairs per CTA: at most one pointwise item (pair, frequency) per thread (PB n_k <= 256,
-// PB <= 32); the smallest PB whose grid still fits one wave of 3 CTAs per SM
-// (__launch_bounds__(256, 3)): a CTA's phases are latency-bound, so more CTAs in flight
-// help until a second, nearly empty wave would start
+// PB <= 32); the smallest PB whose grid still fits one wave of resident CTAs
+// (__launch_bounds__: 3 per SM, 2 at n_k = 128): a CTA's phases are latency-bound, so
+// more CTAs in flight help until a second, nearly empty wave would start
 static int sigma_fft_pb(int nk, int npairs, int sms) {
     int pb = SIGMA_THREADS / nk;
     pb = pb > 32 ? 32 : (pb < 1 ? 1 : pb);
-    while (pb > 1 && (npairs + pb / 2 - 1) / (pb / 2) <= 3 * sms) pb >>= 1;
+    const int occ = nk >= 128 ? 2 : 3;
+    while (pb > 1 && (npairs + pb / 2 - 1) / (pb / 2) <= occ * sms) pb >>= 1;
     return pb;
 }
-// DIF (forward, w^{-1}) or DIT (inverse, w^{+1}) radix-2 passes over one line of
-// NK = 2^LG points, TL = 2^LTL threads per line (consecutive lanes of one warp)
-template <int LG, bool INV>
-__device__ __forceinline__ void fft_line(cplx* d, const cplx* tw, int tl, int LTL, bool active) {
-    constexpr int NK = 1 << LG;
+__host__ __device__ constexpr int brev_c(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+    return r;
+}
+// R-point DFT of v in registers (R <= 16), natural order in and out; tw[j * ts] = w_R^{-j}
+// (conjugated for the inverse).  Radix-2 decimation in frequency with compile-time
+// indices, then the bit-reversal as register renaming.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_small(cplx* v, const cplx* tw, int ts) {
 #pragma unroll
-    for (int st = 0; st < LG; ++st) {
-        const int ls = INV ? st : LG - 1 - st;   // log2 of the butterfly span
-        const int s = 1 << ls;
-        if (active) {
-            for (int j = tl; j < NK / 2; j += 1 << LTL) {
-                const int r = j & (s - 1), a = ((j - r) << 1) + r, bb = a + s;
-                const cplx w = tw[r << (LG - 1 - ls)];
-                const cplx x = d[a];
-                if (!INV) {
-                    const cplx y = d[bb];
-                    d[a] = cadd(x, y);
-                    d[bb] = cmul(csub(x, y), w);
-                } else {
-                    const cplx y = cmul(d[bb], cconj(w));
-                    d[a] = cadd(x, y);
-                    d[bb] = csub(x, y);
-                }
+    for (int s = R / 2; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int j = 0; j < R / 2; ++j) {
+            const int r = j % s, a = (j / s) * 2 * s + r, b = a + s;
+            const cplx x = v[a], y = v[b];
+            v[a] = cadd(x, y);
+            const cplx d = csub(x, y);
+            if (r == 0) {
+                v[b] = d;
+            } else {
+                const cplx w = tw[r * (R / (2 * s)) * ts];
+                v[b] = cmul(d, INV ? cconj(w) : w);
             }
         }
-        __syncwarp();   // every lane takes part (a line's TL threads share one warp)
     }
+    constexpr int bits = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : R == 2 ? 1 : 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = brev_c(i, bits);
+        if (j > i) { const cplx t = v[i]; v[i] = v[j]; v[j] = t; }
+    }
+}
+// one transform of every line (forward or inverse), natural order in place
+template <int LG, bool INV>
+__device__ __forceinline__ void fft_lines(cplx* dat, const cplx* tw, int nlines) {
+    constexpr int NK = 1 << LG, R1 = fft_r1(LG), R2 = fft_r2(LG);
+    const int LS = fft_ls(LG), tid = threadIdx.x;
+    // pass 1: (line, n2) tasks, in place
+    for (int t = tid; t < nlines * R2; t += SIGMA_THREADS) {
+        cplx* L = dat + (t / R2) * LS;
+        const int n2 = t % R2;
+        cplx v[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) v[n1] = L[fft_pad(R2 * n1 + n2, LG)];
+        dft_small<R1, INV>(v, tw, NK / R1);
+#pragma unroll
+        for (int f1 = 1; f1 < R1; ++f1) {
+            if (R2 > 1 && n2) {
+                const cplx w = tw[(f1 * n2) & (NK - 1)];
+                v[f1] = cmul(v[f1], INV ? cconj(w) : w);
+            }
+        }
+#pragma unroll
+        for (int f1 = 0; f1 < R1; ++f1) L[fft_pad(R2 * f1 + n2, LG)] = v[f1];
+    }
+    __syncthreads();
+    if (R2 == 1) return;
+    // pass 2: (line, f1) tasks, all reads before the writes; T2 per thread at most
+    // (8 PB R1 with PB <= min(32, 256 / n_k), sigma_fft_pb)
+    constexpr int PBMAX = 256 / NK < 32 ? 256 / NK : 32;
+    constexpr int T2 = 8 * PBMAX * R1 / SIGMA_THREADS > 1 ? 8 * PBMAX * R1 / SIGMA_THREADS : 1;
+    cplx v[T2][R2];
+#pragma unroll
+    for (int u = 0; u < T2; ++u) {
+        const int t = tid + u * SIGMA_THREADS;
+        if (t < nlines * R1) {
+            const cplx* L = dat + (t / R1) * LS;
+            const int f1 = t % R1;
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) v[u][n2] = L[fft_pad(R2 * f1 + n2, LG)];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < T2; ++u) {
+        const int t = tid + u * SIGMA_THREADS;
+        if (t < nlines * R1) {
+            cplx* L = dat + (t / R1) * LS;
+            const int f1 = t % R1;
+            dft_small<R2, INV>(v[u], tw, NK / R2);
+#pragma unroll
+            for (int f2 = 0; f2 < R2; ++f2) L[fft_pad(f1 + R1 * f2, LG)] = v[u][f2];
+        }
+    }
+    __syncthreads();
 }
 __host__ __device__ __forceinline__ int ilog2(int v) { int l = 0; while ((1 << (l + 1)) <= v) ++l; return l; }
 template <int LG>
-__global__ void __launch_bounds__(SIGMA_THREADS, 3) sigma_fft_kernel(kbe_problem P, int n, int it, int PB) {
+__global__ void __launch_bounds__(SIGMA_THREADS, LG >= 7 ? 2 : 3) sigma_fft_kernel(kbe_problem P, int n, int it, int PB) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
     if (kbe_skip(P, ctl, it)) return;
     extern __shared__ cplx sm[];
     constexpr int NK = 1 << LG;
-    const int LPB = ilog2(PB), TL = fft_tl(NK, PB), LTL = ilog2(TL), LS = fft_ls(NK, PB);
+    const int LPB = ilog2(PB), LS = fft_ls(LG);
     cplx* tw = sm;                        // w^{-j}, j < n_k
     cplx* dat = sm + NK;                  // [PB * 8 lines][LS]
     cplx* det = dat + PB * 8 * LS;        // [PB][2][n_k]: c det V1^(f), c det V2^(f)
@@ -734,43 +801,34 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 3) sigma_fft_kernel(kbe_problem
     // gather: line p*8 + v holds V1_jm (v = jm) or V2_jm (v = 4 + jm) of pair b0 + p
     //   V1 = G<(b,n) = -L(n,b)^dag (b < n) | L(n,n);  V2 = G>(n,b) = -U(n,b)^dag | U(n,n)
     // (p fastest: PB consecutive points of one plane are contiguous)
-    if (sharded(P)) {
-        // gathered buffer: rank chunks of [k_local][capacity slice] + control tail
-        const cplx* src = front_base(P);
-        const int64_t kstride = 8 * plane_len(P.n_steps), rstride = front_chunk(P);
+    {
+        const bool sh = sharded(P);
+        // gathered buffer (k-shards): rank chunks of [k_local][capacity slice] + control tail
+        const cplx* src = sh ? front_base(P) : (const cplx*)P.g_hist + slice_off(n);
+        const int64_t kstride = sh ? 8 * plane_len(P.n_steps) : P.tri, rstride = sh ? front_chunk(P) : 0;
+        const int kper = sh ? nloc : NK;
         for (int i = tid; i < (8 * NK) << LPB; i += SIGMA_THREADS) {
             const int p = i & (PB - 1), c = (i >> LPB) & 7, k = i >> (LPB + 3);
             if (p >= np) continue;
             const int b = b0 + p, cc = c & 3;
-            const cplx v = __ldg(src + (k / nloc) * rstride + (k % nloc) * kstride + sl_idx(c, b));
+            const int kr = sh ? k / kper : 0, kk = sh ? k - kr * kper : k;
+            const cplx v = __ldg(src + kr * rstride + kk * kstride + sl_idx(c, b));
             const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
-            dat[(p * 8 + (c & 4) + jm) * LS + k] = b < n ? cneg(cconj(v)) : v;
-        }
-    } else {
-        const cplx* src = (const cplx*)P.g_hist + slice_off(n);
-        for (int i = tid; i < (8 * NK) << LPB; i += SIGMA_THREADS) {
-            const int p = i & (PB - 1), c = (i >> LPB) & 7, k = i >> (LPB + 3);
-            if (p >= np) continue;
-            const int b = b0 + p, cc = c & 3;
-            const cplx v = __ldg(src + k * P.tri + sl_idx(c, b));
-            const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
-            dat[(p * 8 + (c & 4) + jm) * LS + k] = b < n ? cneg(cconj(v)) : v;
+            dat[(p * 8 + (c & 4) + jm) * LS + fft_pad(k, LG)] = b < n ? cneg(cconj(v)) : v;
         }
     }
     __syncthreads();
-    const int line = tid >> LTL, tl = tid & (TL - 1);
-    const bool has_line = line < np * 8;
-    fft_line<LG, false>(dat + (has_line ? line : 0) * LS, tw, tl, LTL, has_line);
-    __syncthreads();
-    // pointwise Sigma^ in bit-reversed positions q (f = brev(q)), in place: comp 0 -> lines
-    // 0..3, comp 1 -> lines 4..7.  Threads walk q (conflict-free); the partner -f sits at
-    // brev(-f), whose low bits are the top bits of -f, so a quarter-warp's partner reads
-    // also hit distinct banks.
+    fft_lines<LG, false>(dat, tw, np * 8);
+    // pointwise Sigma^ (natural order): dets at f, then every thread reads its partner
+    // -f = n_k - f before any thread overwrites its own f (comp 0 -> lines 0..3,
+    // comp 1 -> lines 4..7)
     const double inv3 = 1.0 / ((double)NK * (double)NK * (double)NK);
     const double un = P.u_table[n];
-    for (int i = tid; i < np * NK; i += SIGMA_THREADS) {
-        const int p = i >> LG, q = i & (NK - 1);
-        const cplx* L = dat + p * 8 * LS + q;
+    const bool act = tid < np * NK;
+    const int p = act ? tid >> LG : 0, q = act ? tid & (NK - 1) : 0;
+    const int pq = fft_pad(q, LG), pg = fft_pad((NK - q) & (NK - 1), LG);
+    if (act) {
+        const cplx* L = dat + p * 8 * LS + pq;
         const double c = (P.u_table[b0 + p] * un) * inv3;
         const cplx d1 = csub(cmul(L[0], L[3 * LS]), cmul(L[LS], L[2 * LS]));
         const cplx d2 = csub(cmul(L[4 * LS], L[7 * LS]), cmul(L[5 * LS], L[6 * LS]));
@@ -779,53 +837,214 @@ __global__ void __launch_bounds__(SIGMA_THREADS, 3) sigma_fft_kernel(kbe_problem
     }
     __syncthreads();
     {
-        constexpr int IT = 1;   // items per thread: np n_k <= 256 (sigma_fft_pb)
-        cplx m1[IT][4], m2[IT][4];
+        cplx m1[4], m2[4];
+        if (act) {
+            const cplx* L = dat + p * 8 * LS + pg;
 #pragma unroll
-        for (int u = 0; u < IT; ++u) {
-            const int i = tid + u * SIGMA_THREADS;
-            if (i < np * NK) {
-                const int p = i >> LG, q = i & (NK - 1);
-                const int f = (int)(__brev((unsigned)q) >> (32 - LG));
-                const int g = (NK - f) & (NK - 1);
-                const int qg = (int)(__brev((unsigned)g) >> (32 - LG));
-                const cplx* L = dat + p * 8 * LS + qg;
-#pragma unroll
-                for (int v = 0; v < 4; ++v) { m1[u][v] = L[v * LS]; m2[u][v] = L[(4 + v) * LS]; }
-            }
+            for (int v = 0; v < 4; ++v) { m1[v] = L[v * LS]; m2[v] = L[(4 + v) * LS]; }
         }
         __syncthreads();
+        if (act) {
+            cplx* L = dat + p * 8 * LS + pq;
+            const cplx d1 = det[(p * 2) * NK + q], d2 = det[(p * 2 + 1) * NK + q];
 #pragma unroll
-        for (int u = 0; u < IT; ++u) {
-            const int i = tid + u * SIGMA_THREADS;
-            if (i < np * NK) {
-                const int p = i >> LG, q = i & (NK - 1);
-                cplx* L = dat + p * 8 * LS + q;
-                const cplx d1 = det[(p * 2) * NK + q], d2 = det[(p * 2 + 1) * NK + q];
-#pragma unroll
-                for (int jm = 0; jm < 4; ++jm) {
-                    const int o = jm == 0 ? 3 : (jm == 3 ? 0 : jm);   // (m'j') of (jm)
-                    cplx s0 = cmul(d1, m2[u][o]), s1 = cmul(d2, m1[u][o]);
-                    if (jm == 1 || jm == 2) { s0 = cneg(s0); s1 = cneg(s1); }
-                    L[jm * LS] = s0;
-                    L[(4 + jm) * LS] = s1;
-                }
+            for (int jm = 0; jm < 4; ++jm) {
+                const int o = jm == 0 ? 3 : (jm == 3 ? 0 : jm);   // (m'j') of (jm)
+                cplx s0 = cmul(d1, m2[o]), s1 = cmul(d2, m1[o]);
+                if (jm == 1 || jm == 2) { s0 = cneg(s0); s1 = cneg(s1); }
+                L[jm * LS] = s0;
+                L[(4 + jm) * LS] = s1;
             }
         }
     }
     __syncthreads();
-    fft_line<LG, true>(dat + (has_line ? line : 0) * LS, tw, tl, LTL, has_line);
-    __syncthreads();
+    fft_lines<LG, true>(dat, tw, np * 8);
     // comp 0 (lines 0..3) -> S<(t_b,t_n) = upper planes 4..7; comp 1 -> S>(t_n,t_b) = planes 0..3
+    cplx* dst = (cplx*)P.s_hist + slice_off(n);
+    for (int i = tid; i < (8 * nloc) << LPB; i += SIGMA_THREADS) {
+        const int pp = i & (PB - 1), v = (i >> LPB) & 7, kl = i >> (LPB + 3);
+        if (pp >= np) continue;
+        const int plane = v < 4 ? 4 + v : v - 4;
+        dst[(int64_t)kl * P.tri + sl_idx(plane, b0 + pp)] = dat[(pp * 8 + v) * LS + fft_pad(P.k_lo + kl, LG)];
+    }
+}
+#define KBE_FFT_LGS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7)
+
+// ---- K1 as DFT GEMMs on the FP64 tensor cores (any even n_k) --------------------------
+// The same Fourier-space Sigma^ as sigma_fft_kernel, with both transforms written as
+// dense complex GEMMs against the n_k x n_k DFT matrix W[f][k] = w^{-fk}, the shared
+// operand of every line (SURVEY 8(a) a11 variant (b), "DFT-as-GEMM"):
+//   forward  V^[f][line] = sum_k W[f][k] V[k][line]                 (M = n_k, N = 8 PB, K = n_k)
+//   inverse  Sigma[k][line] = sum_f conj(W)[k][f] S^[f][line], k local (M = n_k_local)
+// Each 8x8 output tile is one warp's chain of mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4):
+// a complex MAC is 4 real DMMAs (Re += Wr Vr - Wi Vi, Im += Wr Vi + Wi Vr).  W is never
+// stored: the A fragment is looked up in the w^{-j} table at (f k) mod n_k, advanced by
+// 4f per k-step.  16 n_k^2 complex MACs per pair (half the correlations' 32 n_k^2), all
+// on the tensor pipe.  Production path for n_k that is not a power of two; for powers of
+// two the FFT kernel does O(n_k log n_k) and is kept (KBE_SIGMA=dft selects this one).
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__host__ __device__ __forceinline__ int pow2ceil(int v) { int p = 1; while (p < v) p <<= 1; return p; }
+__host__ __device__ __forceinline__ int dft_m8(int nk) { return (nk + 7) & ~7; }
+// line stride (16-byte slots) = 4 mod 8: the B fragment's 8 lines x 4 consecutive k of a
+// quarter-warp hit distinct banks
+__host__ __device__ __forceinline__ int dft_ls(int nk) { return dft_m8(nk) + 4; }
+static size_t sigma_dft_smem(int nk, int pb) {
+    return ((size_t)nk + (size_t)pb * 8 * dft_ls(nk) + (size_t)pb * 2 * nk) * sizeof(cplx);
+}
+// pairs per CTA: PB m8 <= 256 (<= 32 8x8 tiles per GEMM, 4 per warp), halved while the
+// grid stays within one wave of 2 CTAs per SM
+static int sigma_dft_pb(int nk, int npairs, int sms) {
+    int pb = SIGMA_THREADS / pow2ceil(dft_m8(nk) > nk ? dft_m8(nk) : nk);
+    pb = pb > 32 ? 32 : (pb < 1 ? 1 : pb);
+    while (pb > 1 && (npairs + pb / 2 - 1) / (pb / 2) <= 2 * sms) pb >>= 1;
+    return pb;
+}
+#define DFT_TPW 4   // 8x8 tiles per warp and GEMM
+// One complex GEMM pass over the CTA's lines: rows r (f, or local k on the inverse) of
+// the DFT matrix (conjugated when INV) times the lines' first K4 entries.  Results stay
+// in registers (cr/ci: real/imag accumulator pairs of DFT_TPW tiles) until every warp
+// has read its operands; the caller syncs and stores.
+template <bool INV>
+__device__ __forceinline__ void dft_gemm(const cplx* tw, const cplx* dat, int nk, int LS, int row0, int mt, int ncol8,
+                                         double (*cr)[2], double (*ci)[2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int K4 = (nk + 3) & ~3;
+#pragma unroll
+    for (int u = 0; u < DFT_TPW; ++u) {
+        cr[u][0] = cr[u][1] = ci[u][0] = ci[u][1] = 0.0;
+        const int t = warp + 8 * u;
+        if (t >= mt * ncol8) continue;   // warp-uniform
+        const int r = row0 + (t % mt) * 8 + (lane >> 2);         // A row (global f or k)
+        const cplx* B = dat + ((t / mt) * 8 + (lane >> 2)) * LS;  // B column = one line
+        const int kq = lane & 3;
+        const int rr = r % nk;
+        int idx = (rr * kq) % nk;                                 // (r k) mod n_k, k = k0 + kq
+        const int step = (4 * rr) % nk;
+        for (int k0 = 0; k0 < K4; k0 += 4) {
+            const cplx w = tw[idx];
+            const cplx v = B[k0 + kq];
+            const double wr = w.x, wi = INV ? -w.y : w.y;
+            dmma884(cr[u][0], cr[u][1], wr, v.x);
+            dmma884(cr[u][0], cr[u][1], -wi, v.y);
+            dmma884(ci[u][0], ci[u][1], wr, v.y);
+            dmma884(ci[u][0], ci[u][1], wi, v.x);
+            idx += step;
+            if (idx >= nk) idx -= nk;
+        }
+    }
+}
+// store a GEMM's tiles into the lines: entry row - row0 of line c (rows < rmax)
+__device__ __forceinline__ void dft_put(cplx* dat, int LS, int mt, int ncol8, int rmax, double (*cr)[2],
+                                        double (*ci)[2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int u = 0; u < DFT_TPW; ++u) {
+        const int t = warp + 8 * u;
+        if (t >= mt * ncol8) continue;
+        const int r = (t % mt) * 8 + (lane >> 2);
+        if (r >= rmax) continue;
+        const int c = (t / mt) * 8 + 2 * (lane & 3);
+        dat[c * LS + r] = make_double2(cr[u][0], ci[u][0]);
+        dat[(c + 1) * LS + r] = make_double2(cr[u][1], ci[u][1]);
+    }
+}
+__global__ void __launch_bounds__(SIGMA_THREADS, 2) sigma_dft_kernel(kbe_problem P, int n, int it, int PB) {
+    pdl_enter();
+    const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
+    p2p_wait(P);   // the frontier and the control tails of the last update, all ranks
+    if (kbe_skip(P, ctl, it)) return;
+    extern __shared__ cplx sm[];
+    const int nk = P.n_k, LS = dft_ls(nk), LPB = ilog2(PB);
+    cplx* tw = sm;                        // w^{-j}, j < n_k
+    cplx* dat = sm + nk;                  // [PB * 8 lines][LS]
+    cplx* det = dat + PB * 8 * LS;        // [PB][2][n_k]
+    const int b0 = blockIdx.x * PB, np = min(PB, n + 1 - b0);
+    const int nloc = P.k_hi - P.k_lo;
+    const int tid = threadIdx.x;
+    for (int j = tid; j < nk; j += SIGMA_THREADS) {
+        double sn, cs;
+        sincospi(-2.0 * (double)j / (double)nk, &sn, &cs);
+        tw[j] = make_double2(cs, sn);
+    }
+    // lines of absent pairs and the K padding (k in [n_k, K4)) stay zero
+    for (int i = tid; i < PB * 8 * LS; i += SIGMA_THREADS) dat[i] = cz();
+    __syncthreads();
+    {
+        const bool sh = sharded(P);
+        const cplx* src = sh ? front_base(P) : (const cplx*)P.g_hist + slice_off(n);
+        const int64_t kstride = sh ? 8 * plane_len(P.n_steps) : P.tri, rstride = sh ? front_chunk(P) : 0;
+        const int kper = sh ? nloc : nk;
+        for (int i = tid; i < (8 * nk) << LPB; i += SIGMA_THREADS) {
+            const int p = i & (PB - 1), c = (i >> LPB) & 7, k = i >> (LPB + 3);
+            if (p >= np) continue;
+            const int b = b0 + p, cc = c & 3;
+            const cplx v = __ldg(src + (k / kper) * rstride + (k % kper) * kstride + sl_idx(c, b));
+            const int jm = b < n ? ((cc & 1) * 2 + (cc >> 1)) : cc;
+            dat[(p * 8 + (c & 4) + jm) * LS + k] = b < n ? cneg(cconj(v)) : v;
+        }
+    }
+    __syncthreads();
+    double cr[DFT_TPW][2], ci[DFT_TPW][2];
+    const int mt = dft_m8(nk) / 8;
+    dft_gemm<false>(tw, dat, nk, LS, 0, mt, PB, cr, ci);
+    __syncthreads();
+    dft_put(dat, LS, mt, PB, nk, cr, ci);
+    __syncthreads();
+    // pointwise Sigma^ in natural order (f and -f = n_k - f), as in sigma_fft_kernel
+    const double inv3 = 1.0 / ((double)nk * (double)nk * (double)nk);
+    const double un = P.u_table[n];
+    for (int i = tid; i < np * nk; i += SIGMA_THREADS) {
+        const int p = i / nk, q = i % nk;
+        const cplx* L = dat + p * 8 * LS + q;
+        const double c = (P.u_table[b0 + p] * un) * inv3;
+        const cplx d1 = csub(cmul(L[0], L[3 * LS]), cmul(L[LS], L[2 * LS]));
+        const cplx d2 = csub(cmul(L[4 * LS], L[7 * LS]), cmul(L[5 * LS], L[6 * LS]));
+        det[(p * 2) * nk + q] = cscale(d1, c);
+        det[(p * 2 + 1) * nk + q] = cscale(d2, c);
+    }
+    __syncthreads();
+    {
+        const int i = tid;   // np n_k <= 256 (sigma_dft_pb)
+        cplx m1[4], m2[4];
+        const bool act = i < np * nk;
+        const int p = act ? i / nk : 0, q = act ? i % nk : 0;
+        if (act) {
+            const cplx* L = dat + p * 8 * LS + (q ? nk - q : 0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) { m1[v] = L[v * LS]; m2[v] = L[(4 + v) * LS]; }
+        }
+        __syncthreads();
+        if (act) {
+            cplx* L = dat + p * 8 * LS + q;
+            const cplx d1 = det[(p * 2) * nk + q], d2 = det[(p * 2 + 1) * nk + q];
+#pragma unroll
+            for (int jm = 0; jm < 4; ++jm) {
+                const int o = jm == 0 ? 3 : (jm == 3 ? 0 : jm);
+                cplx s0 = cmul(d1, m2[o]), s1 = cmul(d2, m1[o]);
+                if (jm == 1 || jm == 2) { s0 = cneg(s0); s1 = cneg(s1); }
+                L[jm * LS] = s0;
+                L[(4 + jm) * LS] = s1;
+            }
+        }
+    }
+    __syncthreads();
+    const int mt2 = (nloc + 7) / 8;
+    dft_gemm<true>(tw, dat, nk, LS, P.k_lo, mt2, PB, cr, ci);
+    __syncthreads();
+    dft_put(dat, LS, mt2, PB, nloc, cr, ci);
+    __syncthreads();
     cplx* dst = (cplx*)P.s_hist + slice_off(n);
     for (int i = tid; i < (8 * nloc) << LPB; i += SIGMA_THREADS) {
         const int p = i & (PB - 1), v = (i >> LPB) & 7, kl = i >> (LPB + 3);
         if (p >= np) continue;
         const int plane = v < 4 ? 4 + v : v - 4;
-        dst[(int64_t)kl * P.tri + sl_idx(plane, b0 + p)] = dat[(p * 8 + v) * LS + P.k_lo + kl];
+        dst[(int64_t)kl * P.tri + sl_idx(plane, b0 + p)] = dat[(p * 8 + v) * LS + kl];
     }
 }
-#define KBE_FFT_LGS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7)
 
 // kernel-level sigma_slice API on batch-last (n_k,2,2,nb) buffers; one CTA per pair.
 __global__ void __launch_bounds__(256) sigma_slice_kernel(int nk, int nb, const cplx* gpi, const cplx* gri,
@@ -2876,6 +3095,7 @@ static int ensure_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(sigma_frontier_kernel<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) { set_err("cudaFuncSetAttribute(sigma_frontier)", e); return KBE_ERR_CUDA; }
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sigma_dft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 #define KBE_FFT_ATTR(L) if (e == cudaSuccess) e = cudaFuncSetAttribute(sigma_fft_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     KBE_FFT_LGS(KBE_FFT_ATTR)
 #undef KBE_FFT_ATTR
@@ -2937,13 +3157,22 @@ static int check_problem(const kbe_problem* p) {
 }
 
 // ---- launch specs of the step kernels (shared by the stream and graph paths)
-static int g_sigma_direct = -1;   // KBE_SIGMA_DIRECT=1: the O(n_k^2) correlation kernel (A/B)
+// K1 variant: KBE_SIGMA = fft (default for power-of-two n_k) | dft (DMMA DFT GEMMs, the
+// default otherwise) | direct (the O(n_k^2) correlation kernel), for A/B runs
+static int g_sigma_kind = -1;   // 0 auto, 1 fft, 2 dft, 3 direct
 static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
-    if (g_sigma_direct < 0) {
-        const char* e = getenv("KBE_SIGMA_DIRECT");
-        g_sigma_direct = (e && e[0] == '1') ? 1 : 0;
+    if (g_sigma_kind < 0) {
+        const char* e = getenv("KBE_SIGMA");
+        g_sigma_kind = !e ? 0 : !strcmp(e, "fft") ? 1 : !strcmp(e, "dft") ? 2 : !strcmp(e, "direct") ? 3 : 0;
     }
-    if (sigma_fft_ok(p->n_k) && !g_sigma_direct) {
+    const bool fft = sigma_fft_ok(p->n_k) && (g_sigma_kind == 0 || g_sigma_kind == 1);
+    if (!fft && g_sigma_kind != 3) {
+        const int pb = sigma_dft_pb(p->n_k, n + 1, g_num_sms);
+        make_spec(s, sigma_dft_kernel, dim3((n + 1 + pb - 1) / pb), dim3(SIGMA_THREADS), sigma_dft_smem(p->n_k, pb),
+                  *p, n, it, pb);
+        return;
+    }
+    if (fft) {
         const int pb = sigma_fft_pb(p->n_k, n + 1, g_num_sms);
         const dim3 grid((n + 1 + pb - 1) / pb), block(SIGMA_THREADS);
         const size_t smem = sigma_fft_smem(p->n_k, pb);
@@ -3418,6 +3647,12 @@ int kbe_launches_per_eval(const kbe_problem* p) {
 }
 int64_t kbe_ctl_hf_sum_offset(void) { return (int64_t)offsetof(kbe_ctl, hf_sum); }
 int32_t kbe_max_n_k(void) { return KBE_MAX_NK; }
+int kbe_set_sigma_variant(int32_t kind) {
+    if (kind < 0 || kind > 3) return -1;
+    const int prev = g_sigma_kind < 0 ? 0 : g_sigma_kind;
+    g_sigma_kind = kind;
+    return prev;
+}
 
 int kbe_run(const kbe_problem* p, int32_t n_first, int32_t n_last, int32_t use_graph, void* stream) {
     int rc = check_problem(p);

@@ -356,6 +356,18 @@ def _incremental_default(n_k: int) -> bool:
     return n_k >= 8
 
 
+_SIGMA_VARIANTS = {"auto": 0, "fft": 1, "dft": 2, "direct": 3}
+
+
+def _sigma_variant_from_env() -> None:
+    """KBE_SIGMA = auto | fft | dft | direct selects the K1 kernel (kbe_set_sigma_variant):
+    FFT for power-of-two n_k and DMMA DFT GEMMs otherwise by default."""
+    env = os.environ.get("KBE_SIGMA", "auto")
+    if env not in _SIGMA_VARIANTS:
+        raise ConfigError(f"KBE_SIGMA must be one of {sorted(_SIGMA_VARIANTS)}, got {env!r}")
+    _lib.lib().kbe_set_sigma_variant(_SIGMA_VARIANTS[env])
+
+
 def _dist_info(schedule: Schedule):
     """(rank, world) of the k-shard group: torch.distributed when initialised."""
     import torch.distributed as dist
@@ -398,6 +410,7 @@ class PropagationDriver:
         self.k_lo, self.k_hi = shard_range(grid.n_k, self.rank, self.world)
         dev = require_cuda()
         self.device = dev
+        _sigma_variant_from_env()
         tri = _lib.tri_size(capacity)
         nkl = self.k_hi - self.k_lo
         g_hist = torch.empty((nkl, tri), dtype=torch.complex128, device=dev)

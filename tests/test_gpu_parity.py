@@ -442,3 +442,46 @@ def test_step_timings_from_cuda_events():
     one.timings_enabled = True
     rep = one.step()
     assert rep.timings["collision"] > 0.0 and rep.density == plain[0].density
+
+
+# ------------------------------------------------------------------ K1 variants
+@pytest.mark.parametrize("n_k,variant", [(6, "auto"), (10, "auto"), (12, "auto"), (24, "auto"), (2, "dft"),
+                                         (8, "dft"), (16, "dft"), (32, "dft"), (6, "direct"), (2, "fft"),
+                                         (4, "fft"), (8, "fft"), (16, "fft"), (32, "fft"), (128, "fft"),
+                                         (128, "dft")])
+def test_sigma_variant_trajectory_matches_oracle(n_k, variant, monkeypatch):
+    """K1 as FFTs (power-of-two n_k), as DMMA DFT GEMMs (any even n_k; the default when n_k
+    is not a power of two) and as the direct correlations all reproduce the oracle's
+    trajectory, G and Sigma, to 1e-10 (selfenergy.py:59-325)."""
+    monkeypatch.setenv("KBE_SIGMA", variant)
+    n_steps = 25
+    model = kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.1)
+    drv = kb.PropagationDriver(kb.build_kgrid(n_k), model, kb.StepConfig(dt=0.02, n_steps=n_steps))
+    reps = drv.run()
+    ref = O.OracleDriver(n_k, O.Model(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.1), 0.02, n_steps)
+    ref_reps = ref.run()
+    assert rel_err(drv.state.lesser, ref.GL) <= 1e-10
+    assert rel_err(drv.state.greater, ref.GG) <= 1e-10
+    assert rel_err(drv.sigma.lesser, ref.SL) <= 1e-10
+    assert rel_err(drv.sigma.greater, ref.SG) <= 1e-10
+    np.testing.assert_allclose([r.density for r in reps], [r.density for r in ref_reps], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("variant", ["fft", "dft", "direct"])
+def test_sigma_variants_on_nk64_golden(variant, monkeypatch):
+    """The n_k = 64 synthetic golden (the reference's own run) with each K1 variant."""
+    monkeypatch.setenv("KBE_SIGMA", variant)
+    g = load_golden("traj_nk64_synth.npz")
+    drv = _driver_from_fixture(g)
+    drv.run()
+    N = int(g["n_steps"])
+    assert rel_err(drv.state.lesser[:, :, :, N, :], g["final_row_lesser"]) <= 1e-10
+    assert rel_err(drv.state.greater[:, :, :, :, N], g["final_col_greater"]) <= 1e-10
+
+
+def test_sigma_variant_setter_rejects_unknown(monkeypatch):
+    from paper_2505_19467_b200 import _lib
+    assert _lib.lib().kbe_set_sigma_variant(7) == -1
+    monkeypatch.setenv("KBE_SIGMA", "bogus")
+    with pytest.raises(kb.ConfigError):
+        kb.PropagationDriver(kb.build_kgrid(4), kb.ModelConfig(), kb.StepConfig(dt=0.02, n_steps=2))
