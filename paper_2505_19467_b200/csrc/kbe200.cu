@@ -2347,20 +2347,48 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
 // (+ the delta slots after an incremental evaluation); points 0..n-1, and n itself in
 // the corrector (the diagonal's I<(t_n, t_n)).
 // One warp item = 2 points x 4 block entries of one local k (8 outputs, 128 contiguous
-// bytes per slot) x RED_G slot groups: lane g*8 + o sums the slots q = g, g + RED_G, ...
-// of the list [row slots, column slots] in order, RED_BATCH loads in flight; the groups
-// are combined by a fixed xor-shuffle tree.  The summation order depends only on
-// (n, b), so results are bitwise reproducible and independent of the launch shape.
-// Persistent grid, items strided over all warps.
+// bytes per slot) x RED_G slot groups: lane g*8 + o sums, in order, the row slots
+// bc = g, g + RED_G, ... (< b/TB + 1) and then the column slots sc = b/ts + g, ... of a(b),
+// and the gc slots bc = g, ... of g(b); the groups are combined by a fixed xor-shuffle
+// tree.  Each stream is a strided pointer walk with RED_BATCH loads in flight (the row
+// and gc streams interleaved), so the loop is loads and adds only.  The summation order
+// depends only on (n, b): results are bitwise reproducible and independent of the
+// launch shape.  Persistent grid, items strided over all warps.
 #define RED_G 4
 #define RED_BATCH 6
+// acc_a += sum of na slots at pa (stride st), acc_b += nb slots at pb (b stream optional:
+// nb = 0); with D, each slot adds its delta slot at the same offset from da / db
+template <int B, bool D>
+__device__ __forceinline__ void red_streams(const cplx* pa, const cplx* da, int na, const cplx* pb, const cplx* db,
+                                            int nb, int64_t st, cplx& acc_a, cplx& acc_b) {
+    const int nmax = na > nb ? na : nb;
+    for (int q = 0; q < nmax; q += B) {
+        cplx va[B], vb[B], wa[B], wb[B];
+        // every load of the batch is issued unconditionally (index clamped, value masked
+        // afterwards): a branch around a load would serialise the batch
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int64_t ia = (int64_t)min(q + u, na > 0 ? na - 1 : 0) * st;
+            const int64_t ib = (int64_t)min(q + u, nb > 0 ? nb - 1 : 0) * st;
+            va[u] = __ldcg(pa + ia);
+            vb[u] = __ldcg(pb + ib);
+            if (D) { wa[u] = __ldcg(da + ia); wb[u] = __ldcg(db + ib); }
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (D) { va[u] = cadd(va[u], wa[u]); vb[u] = cadd(vb[u], wb[u]); }
+            if (q + u < na) acc_a = cadd(acc_a, va[u]);
+            if (q + u < nb) acc_b = cadd(acc_b, vb[u]);
+        }
+    }
+}
 template <int INC>
 __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
     const int nkl = P.k_hi - P.k_lo;
-    const int64_t N1 = P.n_steps + 1, cs = N1 * 4;
+    const int64_t N1 = P.n_steps + 1, cs = N1 * 4, st = cs * RED_G;
     const int nf = phase == 0 ? n - 1 : n;
     const int npts = phase == 0 ? n : n + 1;
     const int cts = coll_ts(nf, nkl, 0);
@@ -2373,52 +2401,28 @@ __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, in
         const int kl = item / pairs;
         const int b = (item % pairs) * 2 + (o >> 2), c = o & 3;
         cplx a = cz(), gg = cz();
-        int na = 0, ng = 0;
         if (b < npts) {
-            const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c;
-            const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c;
-            const cplx* rowP = (const cplx*)P.row_part + rb;
-            const cplx* colP = (const cplx*)P.col_part + cb;
-            const cplx* gcP = (const cplx*)P.gc_part + rb;
-            const cplx* rowD = (const cplx*)P.row_delta + rb;
-            const cplx* colD = (const cplx*)P.col_delta + cb;
-            const cplx* gcD = (const cplx*)P.gc_delta + rb;
+            const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c + g * cs;
             const int c0 = b / cts;
+            const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c + (int64_t)(c0 + g) * cs;
             const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
-            na = nr + ns;
-            ng = b < nf ? nr : 0;
-            // every load of a batch is issued unconditionally (address clamped to a valid
-            // slot, value masked afterwards): a branch around each load, or an add right
-            // after it, serialises the batch into one round trip per load
-            auto run = [&](auto with_delta) {
-                constexpr bool D = decltype(with_delta)::value;
-                constexpr int NB = D ? RED_BATCH / 2 : RED_BATCH;   // loads in flight: 4 * NB (D) or 2 * NB
-                for (int q0 = g; q0 < na || q0 < ng; q0 += NB * RED_G) {
-                    cplx va[NB], vg[NB], da[NB], dg[NB];
-#pragma unroll
-                    for (int u = 0; u < NB; ++u) {
-                        const int q = q0 + u * RED_G;
-                        const bool rowq = q < nr || q >= na;   // past the list: row slot 0 (masked)
-                        const int64_t oa = q >= na ? 0 : (rowq ? (int64_t)q * cs : (int64_t)(c0 + q - nr) * cs);
-                        const int64_t ogg = q < ng ? (int64_t)q * cs : 0;
-                        va[u] = __ldcg((rowq ? rowP : colP) + oa);
-                        vg[u] = __ldcg(gcP + ogg);
-                        if (D) {
-                            da[u] = __ldcg((rowq ? rowD : colD) + oa);
-                            dg[u] = __ldcg(gcD + ogg);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < NB; ++u) {
-                        const int q = q0 + u * RED_G;
-                        if (D) { va[u] = cadd(va[u], da[u]); vg[u] = cadd(vg[u], dg[u]); }
-                        if (q < na) a = cadd(a, va[u]);
-                        if (q < ng) gg = cadd(gg, vg[u]);
-                    }
-                }
-            };
-            if (INC && dl) run(std::true_type{});
-            else run(std::false_type{});
+            // slots of this lane's group
+            const int mr = nr > g ? (nr - g + RED_G - 1) / RED_G : 0;
+            const int ms = ns > g ? (ns - g + RED_G - 1) / RED_G : 0;
+            const int mg = b < nf ? mr : 0;
+            const cplx* rowP = (const cplx*)P.row_part + rb;
+            const cplx* gcP = (const cplx*)P.gc_part + rb;
+            const cplx* colP = (const cplx*)P.col_part + cb;
+            cplx dummy = cz();
+            if (INC && dl) {
+                red_streams<RED_BATCH / 2, true>(rowP, (const cplx*)P.row_delta + rb, mr, gcP,
+                                                 (const cplx*)P.gc_delta + rb, mg, st, a, gg);
+                red_streams<RED_BATCH / 2, true>(colP, (const cplx*)P.col_delta + cb, ms, colP,
+                                                 (const cplx*)P.col_delta + cb, 0, st, a, dummy);
+            } else {
+                red_streams<RED_BATCH, false>(rowP, nullptr, mr, gcP, nullptr, mg, st, a, gg);
+                red_streams<RED_BATCH, false>(colP, nullptr, ms, colP, nullptr, 0, st, a, dummy);
+            }
         }
         // groups (lanes o, o+8, o+16, o+24): ((g0 + g1) + (g2 + g3)); a + b == b + a exactly
 #pragma unroll
