@@ -119,6 +119,69 @@ __device__ __forceinline__ fcx cfma_cb(fcx a, fcx b, fcx acc) {
 __device__ __forceinline__ fcx cfma_ca(fcx a, fcx b, fcx acc) {
     return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, acc.y)));
 }
+// Packed FP32 (FFMA2, fma.rn.f32x2) complex64 MACs for the incremental collision loop:
+// acc += s c with s a streamed history cell and c a task / slice constant.  s's real and
+// imaginary parts enter as broadcast scalar operands (free in SASS) and c as the pair
+// (c.x, c.y) or its rotation, so one complex MAC is 2 FFMA2 instead of 4 FFMA; the
+// rotations of a loop-invariant c are hoisted by the compiler (one negated register).
+__device__ __forceinline__ fcx ffma2(fcx a, fcx b, fcx c) {
+    unsigned long long A = *reinterpret_cast<unsigned long long*>(&a), B = *reinterpret_cast<unsigned long long*>(&b),
+                       C = *reinterpret_cast<unsigned long long*>(&c);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(C) : "l"(A), "l"(B));
+    return *reinterpret_cast<fcx*>(&C);
+}
+__device__ __forceinline__ fcx bc2(float x) { return make_float2(x, x); }
+// acc += s c = s.x (c.x, c.y) + s.y (-c.y, c.x)           (r = (-c.y, c.x) precomputed)
+__device__ __forceinline__ fcx cm_sc(fcx s, fcx c, fcx r, fcx acc) { return ffma2(bc2(s.y), r, ffma2(bc2(s.x), c, acc)); }
+// acc += conj(s) c = s.x (c.x, c.y) + s.y (c.y, -c.x)     (r = (c.y, -c.x))
+__device__ __forceinline__ fcx cm_Sc(fcx s, fcx c, fcx r, fcx acc) { return ffma2(bc2(s.y), r, ffma2(bc2(s.x), c, acc)); }
+// acc += s conj(c) = s.x (c.x, -c.y) + s.y (c.y, c.x)
+__device__ __forceinline__ fcx cm_sC(fcx s, fcx c, fcx acc) {
+    return ffma2(bc2(s.y), make_float2(c.y, c.x), ffma2(bc2(s.x), make_float2(c.x, -c.y), acc));
+}
+__device__ __forceinline__ fcx rot_p(fcx c) { return make_float2(-c.y, c.x); }   // i c
+__device__ __forceinline__ fcx rot_m(fcx c) { return make_float2(c.y, -c.x); }   // -i c
+// 2x2 blocks: acc += C S (S streamed), acc += C S^dag, acc += S C^dag, acc += S^dag C, acc += S C
+__device__ __forceinline__ void mm2_cs(fcx* acc, const fcx* C, const fcx* Cr, const fcx* S) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) acc[2 * i + j] = cm_sc(S[2 * k + j], C[2 * i + k], Cr[2 * i + k], acc[2 * i + j]);
+}
+__device__ __forceinline__ void mm2_csdag(fcx* acc, const fcx* C, const fcx* Cr, const fcx* S) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) acc[2 * i + j] = cm_Sc(S[2 * j + k], C[2 * i + k], Cr[2 * i + k], acc[2 * i + j]);
+}
+__device__ __forceinline__ void mm2_scdag(fcx* acc, const fcx* S, const fcx* C) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) acc[2 * i + j] = cm_sC(S[2 * i + k], C[2 * j + k], acc[2 * i + j]);
+}
+__device__ __forceinline__ void mm2_sdagc(fcx* acc, const fcx* S, const fcx* C) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) acc[2 * i + j] = cm_Sc(S[2 * k + i], C[2 * k + j], rot_m(C[2 * k + j]), acc[2 * i + j]);
+}
+__device__ __forceinline__ void mm2_sc(fcx* acc, const fcx* S, const fcx* C) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) acc[2 * i + j] = cm_sc(S[2 * i + k], C[2 * k + j], rot_p(C[2 * k + j]), acc[2 * i + j]);
+}
 // Smith's division
 __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
     if (fabs(b.x) >= fabs(b.y)) {
@@ -1668,9 +1731,15 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 front_ab(fr, s, n, w, a, l);
                 front_ab(fp, s, n, w, a0, l0);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) { vec[lane][c] = f32(csub(a[c], a0[c])); vec[lane][4 + c] = f32(csub(l[c], l0[c])); }
+                for (int c = 0; c < 4; ++c) {
+                    const fcx as = f32(csub(a[c], a0[c])), bs = f32(csub(l[c], l0[c]));
+                    vec[lane][c] = as;
+                    vec[lane][4 + c] = bs;
+                    vec[32 + lane][c] = rot_m(as);       // for col += As SU^dag
+                    vec[32 + lane][4 + c] = rot_p(bs);   // for col += Bs SL
+                }
             }
-            fcx Ab[4], Bb[4], col[4];
+            fcx Ab[4], Bb[4], Abr[4], Bbr[4], col[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) { Ab[c] = make_float2(0.f, 0.f); Bb[c] = Ab[c]; col[c] = Ab[c]; }
             const double wb = quad_w(n, b, dt, P.quad);
@@ -1681,6 +1750,8 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { Ab[c] = f32(csub(a[c], a0[c])); Bb[c] = f32(csub(l[c], l0[c])); }
             }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { Abr[c] = rot_p(Ab[c]); Bbr[c] = rot_m(Bb[c]); }
             __syncwarp();
             // OFF: a block strictly below the diagonal (b < s for every lane and slice):
             // no per-slice point tests
@@ -1699,19 +1770,27 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
 #pragma unroll
                 for (int c = 0; c < 4; ++c) row[c] = make_float2(0.f, 0.f);
                 if (OFF || b <= s) {
-                    mm_acc(row, Ab, SU);
+                    mm2_cs(row, Ab, Abr, SU);                 // row += Ab SU
                     if (OFF || b < s) {
-                        mm_bdag_acc(row, Bb, SL);
-                        fcx As[4], Bs[4];
+                        mm2_csdag(row, Bb, Bbr, SL);          // row += Bb SL^dag
+                        fcx As[4], Bs[4], Asr[4], Bsr[4];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) { As[c] = vec[i][c]; Bs[c] = vec[i][4 + c]; }
-                        mm_bdag_acc(col, As, SU);
-                        mm_acc(col, Bs, SL);
+                        for (int c = 0; c < 4; ++c) {
+                            As[c] = vec[i][c];
+                            Bs[c] = vec[i][4 + c];
+                            Asr[c] = vec[32 + i][c];
+                            Bsr[c] = vec[32 + i][4 + c];
+                        }
+                        mm2_csdag(col, As, Asr, SU);          // col += As SU^dag
+                        mm2_cs(col, Bs, Bsr, SL);             // col += Bs SL
                     } else {
                         fcx t[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) t[c] = make_float2(0.f, 0.f);
-                        mm_acc(t, Bb, SL);
+                        fcx Bbp[4];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) Bbp[c] = rot_p(Bb[c]);
+                        mm2_cs(t, Bb, Bbp, SL);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) row[c] = make_float2(row[c].x - t[c].x, row[c].y - t[c].y);
                     }
@@ -1797,14 +1876,14 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 for (int c = 0; c < 4; ++c) { acc[c] = make_float2(0.f, 0.f); t[c] = acc[c]; }
                 if (OFF || b <= j) {
                     const float w = OFF ? ((j & 1) ? w_odd : w_even) : (float)quad_w(j, b, dt, P.quad);
-                    mm_bdag_acc(t, GL, X);             // GL X^dag
+                    mm2_scdag(t, GL, X);               // GL X^dag
                     if (OFF || b < j) {
-                        mm_adag_acc(acc, GU, Y);       // GU^dag Y
+                        mm2_sdagc(acc, GU, Y);         // GU^dag Y
                     } else {
                         fcx u[4];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) u[c] = make_float2(0.f, 0.f);
-                        mm_acc(u, GU, Y);
+                        mm2_sc(u, GU, Y);
 #pragma unroll
                         for (int c = 0; c < 4; ++c) acc[c] = make_float2(-u[c].x, -u[c].y);
                     }
