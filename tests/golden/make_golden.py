@@ -309,6 +309,10 @@ def long_fixture(which):
     cfg = kb.StepConfig(dt=0.02, n_steps=N, memory_budget=1 << 40)
     workers = int(os.environ.get("KBE_GOLDEN_WORKERS", "6"))
     shards = max(d for d in range(1, min(workers, n_k) + 1) if n_k % d == 0)
+    # KBE_GOLDEN_SHARDS: fewer shards replicate less work per step (each shard
+    # recomputes the polarizability, selfenergy.py:292); the results are bitwise
+    # independent of the shard count (SURVEY probe P5)
+    shards = int(os.environ.get("KBE_GOLDEN_SHARDS", shards))
     pool = kb.WorkerPool(workers)
     every = int(os.environ.get("KBE_GOLDEN_SAVE_EVERY", "50"))
     rows_k = np.arange(0, n_k, max(1, n_k // 4))

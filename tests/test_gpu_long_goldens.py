@@ -4,9 +4,10 @@ north_star target), cfg4 (n_k = 32, 400-step prefix of the 4000-step workload) a
 cfg5 (n_k = 128, prefix of the 500-step workload).
 
 Each run goes through the production path (speculative iteration counts, the
-complex64 incremental collision corrections, the split K3 reduction, K1's
-sigma_frontier_kernel at n_k = 32 / 64 / 128) and once more with every evaluation in
-FP64 (KBE_INCR=0).  Tolerances: G< / G> rows, columns and equal-time diagonals
+complex64 incremental collision corrections with packed FFMA2 arithmetic, the split
+K3 reduction, K1's four-step FFT kernel at n_k = 32 / 64 / 128) and once more with
+every evaluation in FP64 (KBE_INCR=0); cfg3 and cfg5 also with K1 as DMMA DFT GEMMs
+(KBE_SIGMA=dft).  Tolerances: G< / G> rows, columns and equal-time diagonals
 <= 1e-10 relative to the largest reference entry (north_star); densities 1e-12
 absolute; iteration-count flips at the eps boundary are allowed (SURVEY finding 9)
 but bounded and reported.
@@ -103,3 +104,10 @@ def test_long_reference_golden_fp64_only(name, monkeypatch):
     err = compare_long_golden(name)
     assert not err["incremental"]
     _check(err)
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg5"])
+def test_long_reference_golden_dmma_sigma(name, monkeypatch):
+    """The same long runs with K1 on the FP64 tensor cores (sigma_dft_kernel)."""
+    monkeypatch.setenv("KBE_SIGMA", "dft")
+    _check(compare_long_golden(name))
