@@ -1261,11 +1261,18 @@ __host__ __device__ __forceinline__ int coll_tiles(int n, int nkl) {
     const int T0 = n / TS + 1, T1 = n >= 1 ? (n - 1) / TS + 1 : 0;
     return (T0 * (T0 + 1) / 2 + T1 * (T1 + 1) / 2) * nkl;
 }
+// k-shards with few local k (a strong-scaled rank): twice the tasks.  Their launches are
+// short, so the queue's tail (the last, partly filled round of tasks) is a larger share
+// than the K3 slot traffic that taller tasks save (profiles/r02/scaling_model_*).
+#ifndef KBE_SMALL_NKL
+#define KBE_SMALL_NKL 8
+#endif
 __host__ __device__ __forceinline__ int coll_ts(int n, int nkl, int limit_mode) {
     if (limit_mode) return TS;
     const int tiles = coll_tiles(n, nkl);
-    if (tiles >= KBE_COLL_TASKS) return KBE_VEC_TS;
-    if (2 * tiles >= KBE_COLL_TASKS) return 16;
+    const int target = nkl <= KBE_SMALL_NKL ? 2 * KBE_COLL_TASKS : KBE_COLL_TASKS;
+    if (tiles >= target) return KBE_VEC_TS;
+    if (2 * tiles >= target) return 16;
     return KBE_COL_CHUNK;
 }
 
