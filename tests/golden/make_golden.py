@@ -1,8 +1,15 @@
 """Generate golden vectors by running the REAL reference (kbesolve 0.1.0).
 
-Run in the build container only (the reference is not on the GPU box):
+Run in the build container (the reference sources are at /root/reference):
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+or on any host that has the unmodified reference installed, e.g. the GPU box's 16
+cores with the driver's offline install (long runs; this is how the 120-step cfg5
+fixture was made, profiles/r02/cfg5_golden_gpubox.log):
+
+    KBE_REFERENCE_SRC=$PWD/baseline/_ref KBE_GOLDEN_OUT=gpurun_out KBE_GOLDEN_WORKERS=16 \
+        KBE_GOLDEN_SHARDS=1 python tests/golden/make_golden.py cfg5
 
 Writes ``tests/golden/*.npz``.  Every fixture stores its inputs alongside
 the reference outputs, so tests never need the reference (or a particular
