@@ -8,6 +8,8 @@ single  : n_k = 8, 40 steps, pulse at step 5 -- the production path: K2 starting
           slots, split K3 (K3a + K3b), speculative iteration counts with rollbacks
 options : n_k = 4, 20 steps each with hf_mode="on", Simpson + U(t) ramp, langreth limits
           (fused K3, langreth K2, hf k-mean kernel), plus the kernel-level operators
+variants: the K1 kernels (round 2): four-step FFT at n_k = 16 and 128, DMMA DFT GEMMs at
+          n_k = 8 (KBE_SIGMA=dft) and n_k = 12 (the default there), direct correlations
 p2p     : 2 ranks sharing cuda:0, k-sharded, the update kernels storing each new slice
           into the peer's buffer (CUDA IPC) with epoch flags, 12 steps
 """
@@ -58,6 +60,19 @@ def options():
     kb.sigma_slice(gl, gg, np.linspace(0.4, 1.2, 5), 0.7, kb.build_kgrid(8))
 
 
+def variants():
+    import torch
+    import paper_2505_19467_b200 as kb
+    torch.cuda.set_device(0)
+    model = kb.ModelConfig(u_protocol=1.0, pulse_intensity=0.2, pulse_center=0.1)
+    for n_k, sig, steps in ((16, "fft", 30), (128, "fft", 8), (8, "dft", 30), (12, "auto", 30), (8, "direct", 20)):
+        os.environ["KBE_SIGMA"] = sig
+        drv = kb.PropagationDriver(kb.build_kgrid(n_k), model, kb.StepConfig(dt=0.02, n_steps=steps))
+        reps = drv.run()
+        print("variant", n_k, sig, len(reps), reps[-1].density)
+        drv.close()
+
+
 def _p2p_worker(rank, world, port):
     import torch
     import torch.distributed as dist
@@ -87,4 +102,4 @@ def p2p():
 
 
 if __name__ == "__main__":
-    {"single": single, "options": options, "p2p": p2p}[sys.argv[1]]()
+    {"single": single, "options": options, "variants": variants, "p2p": p2p}[sys.argv[1]]()

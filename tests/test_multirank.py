@@ -40,22 +40,28 @@ def test_collectives_world2_gloo(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("hf, world, p2p", [("off", 2, "1"), ("on", 2, "1"), ("off", 4, "1"),
-                                            ("off", 2, "0"), ("on", 2, "0")])
-def test_k_sharded_driver_matches_single_rank(tmp_path, hf, world, p2p):
+@pytest.mark.parametrize("hf, world, p2p, sigma, n_k",
+                         [("off", 2, "1", "auto", 8), ("on", 2, "1", "auto", 8), ("off", 4, "1", "auto", 8),
+                          ("off", 2, "0", "auto", 8), ("on", 2, "0", "auto", 8),
+                          ("off", 2, "1", "dft", 8), ("off", 2, "1", "auto", 12), ("off", 4, "0", "direct", 8)])
+def test_k_sharded_driver_matches_single_rank(tmp_path, hf, world, p2p, sigma, n_k):
     """Each exchanged chunk carries the rank's G slice and its convergence record; the
     kernels max-reduce the records over ranks, so iteration counts match exactly.
     p2p=1: the update kernel stores into every peer's buffer (CUDA IPC; the ranks share
-    one GPU here, NVLink peers on a node); p2p=0: all-gather through torch.distributed."""
+    one GPU here, NVLink peers on a node); p2p=0: all-gather through torch.distributed.
+    sigma: the K1 variant reading the gathered frontier (FFT, DMMA DFT GEMMs -- the
+    default for n_k = 12 --, direct correlations)."""
     import paper_2505_19467_b200 as kb
-    n_k, n_steps = 8, 40
+    n_steps = 40
     os.environ["KBE_HF"] = hf
     os.environ["KBE_P2P"] = p2p
+    os.environ["KBE_SIGMA"] = sigma
     try:
         mp.spawn(W.driver_worker, args=(world, _port(), str(tmp_path), n_k, n_steps), nprocs=world, join=True)
     finally:
         os.environ.pop("KBE_HF", None)
         os.environ.pop("KBE_P2P", None)
+        os.environ.pop("KBE_SIGMA", None)
     if p2p == "1":
         assert all(np.load(tmp_path / f"drv{r}.npz")["p2p"] for r in range(world))
     parts = [np.load(tmp_path / f"drv{r}.npz") for r in range(world)]
