@@ -656,9 +656,12 @@ def run_ours(args):
         roof, _ = _collision_roofline(kb, drv, hbm_peak)
         roof["peak_kind"] = peak_kind
         try:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "collision_traffic.json")))
-            roof["traffic"] = traffic.get("bytes_per_launch")
-            roof["traffic_note"] = traffic.get("note")
+            # the ncu capture of this workload (profiles/collision_traffic.json, keyed by
+            # workload); none for workloads without a capture
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "collision_traffic.json"))).get(CFG["workload"][:4])
+            if traffic:
+                roof["traffic"] = traffic.get("bytes_per_launch")
+                roof["traffic_note"] = f"n = {traffic['n']} launch: " + traffic.get("note", "")
         except Exception:
             pass
     if rank == 0 and world == 1 and not args.no_cpu:
