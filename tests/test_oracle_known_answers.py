@@ -91,3 +91,37 @@ def test_free_evolution_is_the_cayley_factor_and_second_order():
         assert rel_err(got, 1j * phi[:, None] ** n[None, :]) <= 1e-13
         errs.append(np.abs(got[:, N] - 1j * np.exp(-1j * ev * T)).max())
     assert 3.5 <= errs[0] / errs[1] <= 4.5
+
+
+def _sigma_fourier(gp, gr, u1, u2):
+    """The Fourier-space form K1 (sigma_fft_kernel / sigma_dft_kernel) evaluates:
+    Sigma^_jm(f) = pref s_jm det(gp^(f)) gr^_{m'j'}(-f), x^(f) = sum_k x[k] e^{-2 pi i f k / n_k},
+    s_jm = +1 (j = m) / -1 (j != m), pref = u1 u2 / n_k^2, followed by the inverse transform."""
+    n = gp.shape[0]
+    GP, GR = np.fft.fft(gp, axis=0), np.fft.fft(gr, axis=0)
+    det = GP[:, 0, 0] * GP[:, 1, 1] - GP[:, 0, 1] * GP[:, 1, 0]
+    GRm = GR[(-np.arange(n)) % n]
+    out = np.empty_like(GP)
+    for j in range(2):
+        for m in range(2):
+            out[:, j, m] = (1 if j == m else -1) * det * GRm[:, 1 - m, 1 - j]
+    return np.fft.ifft(out, axis=0) * (u1 * u2 / n ** 2)
+
+
+@pytest.mark.parametrize("n_k", [2, 4, 6, 8, 12, 16, 64, 128])
+def test_fourier_sigma_identity_matches_direct_sums(n_k):
+    """The algebra behind K1: the factorised second-Born Sigma (P, Sigma1, X, Sigma2 as
+    circular correlations, selfenergy.py:59-203) collapses in Fourier space to one
+    determinant times one reversed transform per frequency.  Checked against the
+    oracle's direct sums at every n_k class the kernels take (powers of two: FFT;
+    others: DFT GEMMs) and, at small n_k, against the brute-force momentum sums."""
+    rng = np.random.default_rng(100 + n_k)
+    shape = (n_k, 2, 2)
+    gp = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    gr = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    want = O.sigma_slice(gp, gr, 0.7, 1.3)
+    got = _sigma_fourier(gp, gr, 0.7, 1.3)
+    assert rel_err(got, want) <= 1e-13
+    if n_k <= 12:
+        s1, s2 = _bf_sigma(gp, gr, 0.7, 1.3, O.k_values(n_k))
+        assert rel_err(got, s1 - s2) <= 1e-13
