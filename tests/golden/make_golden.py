@@ -297,14 +297,57 @@ LONG_RUNS = {
 }
 
 
+def _ckpt_save(ck, drv, n, acc):
+    """Resumable state of the reference driver after step n: the filled [0..n] blocks of
+    G<, G>, Sigma<, Sigma> (everything PropagationDriver.step reads from earlier steps,
+    propagator.py:316-382; its ScratchPool only holds overwritten buffers) and the
+    fixture's accumulators.  Written to a temp dir, then renamed (atomic)."""
+    import shutil
+    tmp = ck + ".tmp"
+    shutil.rmtree(tmp, ignore_errors=True)
+    os.makedirs(tmp)
+    for name, arr in (("GL", drv.state.lesser), ("GG", drv.state.greater),
+                      ("SL", drv.sigma.lesser), ("SG", drv.sigma.greater)):
+        np.save(os.path.join(tmp, name + ".npy"), arr[..., : n + 1, : n + 1])
+    extra = {f"acc_{k}": np.asarray(v) for k, v in acc.items() if not k.startswith("rc_")}
+    for k, v in acc.items():
+        if k.startswith("rc_"):
+            extra[k] = v
+    np.savez(os.path.join(tmp, "acc.npz"), n=np.array(n), **extra)
+    shutil.rmtree(ck, ignore_errors=True)
+    os.rename(tmp, ck)
+    print(f"  checkpoint at step {n} -> {ck}", flush=True)
+
+
+def _ckpt_load(ck, drv):
+    """Restore _ckpt_save's state into a fresh driver; returns (n, accumulators)."""
+    d = np.load(os.path.join(ck, "acc.npz"))
+    n = int(d["n"])
+    for name, arr in (("GL", drv.state.lesser), ("GG", drv.state.greater),
+                      ("SL", drv.sigma.lesser), ("SG", drv.sigma.greater)):
+        arr[..., : n + 1, : n + 1] = np.load(os.path.join(ck, name + ".npy"))
+    drv.state.frontier = n
+    acc = {k[4:]: list(d[k]) for k in d.files if k.startswith("acc_")}
+    acc.update({k: d[k] for k in d.files if k.startswith("rc_")})
+    return n, acc
+
+
 def long_fixture(which):
     """A bench workload run by the REAL reference, checkpointed: every
     KBE_GOLDEN_SAVE_EVERY steps (default 50) the prefix computed so far is written,
     so an interrupted run still leaves a usable golden.  Stores the per-step
     observables, the equal-time diagonals, the final row G<(t_s, .) and column
-    G>(., t_s), and rows/columns of a few k every 100 steps."""
+    G>(., t_s), and rows/columns of a few k every 100 steps.
+
+    Resumable (runs longer than one session or one GPU-box call): with
+    KBE_GOLDEN_CKPT=<dir> the driver state is saved there when KBE_GOLDEN_DEADLINE
+    seconds have passed (or at step KBE_GOLDEN_STOP_AT) and the run exits; a later run
+    with the same directory continues from it.  The continuation is bitwise the
+    uninterrupted run (tests/golden/make_golden.py resume_check)."""
     fname, n_k, N, kind, u = LONG_RUNS[which]
     N = int(os.environ.get("KBE_GOLDEN_STEPS", N))
+    if which not in LONG_RUNS_TARGET:
+        LONG_RUNS_TARGET[which] = LONG_RUNS[which][2]
     grid = kb.build_kgrid(n_k)
     kw = dict(pulse_intensity=0.2, pulse_center=0.5)
     if kind == "synth":
@@ -322,41 +365,92 @@ def long_fixture(which):
     shards = int(os.environ.get("KBE_GOLDEN_SHARDS", shards))
     pool = kb.WorkerPool(workers)
     every = int(os.environ.get("KBE_GOLDEN_SAVE_EVERY", "50"))
+    ck = os.environ.get("KBE_GOLDEN_CKPT")
+    deadline = float(os.environ.get("KBE_GOLDEN_DEADLINE", "inf"))
+    stop_at = int(os.environ.get("KBE_GOLDEN_STOP_AT", "0"))
     rows_k = np.arange(0, n_k, max(1, n_k // 4))
     t0 = time.time()
     drv = kb.PropagationDriver(grid, model, cfg, kb.Schedule(n_shards=shards, workers=workers), pool)
-    reps, rows, cols, row_steps = [], [], [], []
-    for n in range(1, N + 1):
-        reps.append(drv.step())
+    acc = dict(iterations=[], residual=[], drift=[], density=[], row_steps=[], seconds=[0.0])
+    n0 = 0
+    if ck and os.path.exists(os.path.join(ck, "acc.npz")):
+        n0, acc = _ckpt_load(ck, drv)
+        print(f"  resumed {which} at step {n0}", flush=True)
+    rows = [acc[f"rc_rows_{s}"] for s in acc["row_steps"]]
+    cols = [acc[f"rc_cols_{s}"] for s in acc["row_steps"]]
+    sec0 = float(acc["seconds"][0])
+    for n in range(n0 + 1, N + 1):
+        r = drv.step()
+        acc["iterations"].append(r.iterations)
+        acc["residual"].append(r.residual)
+        acc["drift"].append(r.anticommutation_drift)
+        acc["density"].append(r.density)
         st = drv.state
         if n % 100 == 0:
-            row_steps.append(n)
+            acc["row_steps"].append(n)
             rows.append(st.lesser[rows_k, :, :, n, : n + 1].copy())
             cols.append(st.greater[rows_k, :, :, : n + 1, n].copy())
-        if n % every == 0 or n == N:
+        stop = n < N and ((time.time() - t0) > deadline or n == stop_at)
+        if n % every == 0 or n == N or stop:
             idx = np.arange(n + 1)
             out = dict(
                 n_k=np.array(n_k), n_steps=np.array(n), target_steps=np.array(LONG_RUNS[which][2]),
                 dt=np.array(0.02), u=np.array(u), pulse_intensity=np.array(0.2), pulse_center=np.array(0.5),
                 u_protocol=np.asarray(model.u_protocol, dtype=float),
-                iterations=np.array([r.iterations for r in reps]),
-                residual=np.array([r.residual for r in reps]),
-                drift=np.array([r.anticommutation_drift for r in reps]),
-                density=np.array([r.density for r in reps]),
+                iterations=np.array(acc["iterations"]),
+                residual=np.array(acc["residual"]),
+                drift=np.array(acc["drift"]),
+                density=np.array(acc["density"]),
                 diag_lesser=st.lesser[:, :, :, idx, idx],
                 diag_greater=st.greater[:, :, :, idx, idx],
                 final_row_lesser=st.lesser[:, :, :, n, : n + 1],
                 final_col_greater=st.greater[:, :, :, : n + 1, n],
-                rows_k=rows_k, row_steps=np.array(row_steps, dtype=int),
-                ref_seconds=np.array(time.time() - t0), workers=np.array(workers), shards=np.array(shards),
+                rows_k=rows_k, row_steps=np.array(acc["row_steps"], dtype=int),
+                ref_seconds=np.array(sec0 + time.time() - t0), workers=np.array(workers), shards=np.array(shards),
             )
-            for s, r, c in zip(row_steps, rows, cols):
-                out[f"rows_lesser_{s}"] = r
-                out[f"cols_greater_{s}"] = c
+            for s_, r_, c_ in zip(acc["row_steps"], rows, cols):
+                out[f"rows_lesser_{s_}"] = r_
+                out[f"cols_greater_{s_}"] = c_
             if kind == "synth":
                 out["eps_c_table"] = np.asarray(model.eps_c_table)
             _save(fname, **out)
-            print(f"  {which} step {n} {time.time() - t0:.0f}s", flush=True)
+            print(f"  {which} step {n} {sec0 + time.time() - t0:.0f}s", flush=True)
+        if stop and ck:
+            acc["seconds"] = [sec0 + time.time() - t0]
+            for s_, r_, c_ in zip(acc["row_steps"], rows, cols):
+                acc[f"rc_rows_{s_}"] = r_
+                acc[f"rc_cols_{s_}"] = c_
+            _ckpt_save(ck, drv, n, acc)
+            return
+
+
+LONG_RUNS_TARGET = {}
+
+
+def resume_check_fixture():
+    """Bitwise check of the checkpoint/resume path on a small workload: n_k = 4, 210 steps
+    straight vs 117 + resume + 93, across the 100-step row snapshots (raises on any difference)."""
+    import shutil
+    import tempfile
+    LONG_RUNS["_rc"] = ("_resume_check.npz", 4, 210, "plain", 1.0)
+    base = tempfile.mkdtemp()
+    os.environ["KBE_GOLDEN_OUT"] = os.path.join(base, "a")
+    long_fixture("_rc")
+    os.environ["KBE_GOLDEN_OUT"] = os.path.join(base, "b")
+    os.environ["KBE_GOLDEN_CKPT"] = os.path.join(base, "ck")
+    os.environ["KBE_GOLDEN_STOP_AT"] = "117"
+    long_fixture("_rc")
+    os.environ.pop("KBE_GOLDEN_STOP_AT")
+    long_fixture("_rc")
+    a = np.load(os.path.join(base, "a", "_resume_check.npz"))
+    b = np.load(os.path.join(base, "b", "_resume_check.npz"))
+    for k in a.files:
+        if k in ("ref_seconds",):
+            continue
+        if not np.array_equal(a[k], b[k]):
+            raise AssertionError(f"resume differs in {k}")
+    print("resume_check: bitwise identical over", list(a.files))
+    shutil.rmtree(base)
 
 
 def cfg3_fixture():
