@@ -11,6 +11,13 @@ fixture was made, profiles/r02/cfg5_golden_gpubox.log):
     KBE_REFERENCE_SRC=$PWD/baseline/_ref KBE_GOLDEN_OUT=gpurun_out KBE_GOLDEN_WORKERS=16 \
         KBE_GOLDEN_SHARDS=1 python tests/golden/make_golden.py cfg5
 
+Runs longer than one call are chained (long_fixture's checkpoint/resume): each call runs
+until a deadline and saves the reference driver's state on the box's /tmp, the next call
+(on the same box, started within minutes) resumes from it:
+
+    KBE_GOLDEN_CKPT=/tmp/kbe_cfg3_ckpt KBE_GOLDEN_DEADLINE=3000 KBE_GOLDEN_WORKERS=16 \
+        KBE_GOLDEN_SHARDS=16 KBE_REFERENCE_SRC=$PWD/baseline/_ref python tests/golden/make_golden.py cfg3
+
 Writes ``tests/golden/*.npz``.  Every fixture stores its inputs alongside
 the reference outputs, so tests never need the reference (or a particular
 numpy RNG) at run time.  The reference is deterministic bitwise (SURVEY
