@@ -380,6 +380,8 @@ def long_fixture(which):
     drv = kb.PropagationDriver(grid, model, cfg, kb.Schedule(n_shards=shards, workers=workers), pool)
     acc = dict(iterations=[], residual=[], drift=[], density=[], row_steps=[], seconds=[0.0])
     n0 = 0
+    if ck and not os.path.exists(os.path.join(ck, "acc.npz")) and os.path.exists(os.path.join(ck + ".tmp", "acc.npz")):
+        os.rename(ck + ".tmp", ck)   # killed between the (complete) temp write and the rename
     if ck and os.path.exists(os.path.join(ck, "acc.npz")):
         n0, acc = _ckpt_load(ck, drv)
         print(f"  resumed {which} at step {n0}", flush=True)
