@@ -433,7 +433,9 @@ def _sigma_variant(n_k):
     """The K1 kernel a launch uses (propagator._sigma_variant_from_env / spec_sigma)."""
     env = os.environ.get("KBE_SIGMA", "auto")
     if env == "auto":
-        return "fft" if n_k >= 2 and not (n_k & (n_k - 1)) else "dft"
+        if n_k == 2:
+            return "direct"
+        return "fft" if not (n_k & (n_k - 1)) else "dft"
     return env
 
 

@@ -230,7 +230,8 @@ int64_t kbe_ctl_hf_sum_offset(void);
  * update): the launch count the bench reports.  -1 on an invalid problem. */
 int kbe_launches_per_eval(const kbe_problem* p);
 /* Sigma kernel variant for every later K1 launch of this process (env KBE_SIGMA, read
- * by the driver): 0 auto (FFT for power-of-two n_k, DMMA DFT GEMMs otherwise), 1 FFT,
+ * by the driver): 0 auto (FFT for power-of-two n_k > 2, the correlations at n_k = 2, DMMA DFT
+ * GEMMs otherwise), 1 FFT,
  * 2 DMMA DFT GEMMs, 3 the O(n_k^2) correlation kernel.  Returns the previous setting,
  * -1 for an unknown kind.  Replaces nothing in the reference: its sigma_second
  * (selfenergy.py:139-203) has one algorithm; this selects how K1 computes the same Sigma. */

@@ -3255,8 +3255,11 @@ static void spec_sigma(KSpec& s, const kbe_problem* p, int n, int it) {
         const char* e = getenv("KBE_SIGMA");
         g_sigma_kind = !e ? 0 : !strcmp(e, "fft") ? 1 : !strcmp(e, "dft") ? 2 : !strcmp(e, "direct") ? 3 : 0;
     }
-    const bool fft = sigma_fft_ok(p->n_k) && (g_sigma_kind == 0 || g_sigma_kind == 1);
-    if (!fft && g_sigma_kind != 3) {
+    // auto: FFT for powers of two, except the dimer (n_k = 2), where the whole run is 5 %
+    // faster with the correlation kernel (profiles/r02/bench_cfg1_variants.jsonl: both
+    // are latency-bound there and the correlations have fewer CTA barriers)
+    const bool fft = sigma_fft_ok(p->n_k) && (g_sigma_kind == 1 || (g_sigma_kind == 0 && p->n_k > 2));
+    if (!fft && g_sigma_kind != 3 && !(g_sigma_kind == 0 && p->n_k == 2)) {
         const int pb = sigma_dft_pb(p->n_k, n + 1, g_num_sms);
         make_spec(s, sigma_dft_kernel, dim3((n + 1 + pb - 1) / pb), dim3(SIGMA_THREADS), sigma_dft_smem(p->n_k, pb),
                   *p, n, it, pb);

@@ -361,7 +361,8 @@ _SIGMA_VARIANTS = {"auto": 0, "fft": 1, "dft": 2, "direct": 3}
 
 def _sigma_variant_from_env() -> None:
     """KBE_SIGMA = auto | fft | dft | direct selects the K1 kernel (kbe_set_sigma_variant):
-    FFT for power-of-two n_k and DMMA DFT GEMMs otherwise by default."""
+    by default FFT for power-of-two n_k > 2, the correlations at n_k = 2 and DMMA DFT GEMMs
+    otherwise."""
     env = os.environ.get("KBE_SIGMA", "auto")
     if env not in _SIGMA_VARIANTS:
         raise ConfigError(f"KBE_SIGMA must be one of {sorted(_SIGMA_VARIANTS)}, got {env!r}")
