@@ -232,6 +232,24 @@ def test_poisoned_state_raises():
         drv.run()
 
 
+@pytest.mark.parametrize("n_k,n_steps", [(2, 3), (4, 40), (16, 33)])
+def test_init_state_is_the_reference_ground_state(n_k, n_steps):
+    """init_state (ref state.py:56-87): G<(0,0)_00 = i, G>(0,0)_11 = -i for every k, zero
+    elsewhere, in the packed layout's slice 0 -- and the same history kbe_init_history
+    gives the driver."""
+    st = kb.init_state(kb.build_kgrid(n_k), n_steps, 0.02)
+    want_l = np.zeros((n_k, 2, 2, n_steps + 1, n_steps + 1), dtype=complex)
+    want_g = np.zeros_like(want_l)
+    want_l[:, 0, 0, 0, 0] = 1.0j
+    want_g[:, 1, 1, 0, 0] = -1.0j
+    assert np.array_equal(st.lesser, want_l)
+    assert np.array_equal(st.greater, want_g)
+    drv = kb.PropagationDriver(kb.build_kgrid(n_k), kb.ModelConfig(u_protocol=1.0),
+                               kb.StepConfig(dt=0.02, n_steps=n_steps))
+    assert torch.equal(drv.state.slice_view(0), st.slice_view(0))
+    assert kb.anticommutation_drift(st, 0) == 0.0
+
+
 def kb_slice_entry(s):
     from paper_2505_19467_b200 import _lib
     return _lib.slice_offset(s)
