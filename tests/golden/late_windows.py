@@ -35,9 +35,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.environ.get("KBE_REFERENCE_SRC", os.path.join(ROOT, "baseline", "_ref")))
 
-import kbesolve as ref  # noqa: E402  (the unmodified reference)
 import torch  # noqa: E402
 
 import bench  # noqa: E402  (the workload definition: tables, U, pulse)
@@ -49,13 +47,24 @@ def rel(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
-def main():
-    cfg = dict(bench.WORKLOADS[os.environ.get("KBE_WORKLOAD", "cfg3")])
+def reference():
+    """The unmodified reference (kbesolve 0.1.0): KBE_REFERENCE_SRC, else the driver's
+    offline install baseline/_ref.  ImportError when neither is there."""
+    src = os.environ.get("KBE_REFERENCE_SRC", os.path.join(ROOT, "baseline", "_ref"))
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    import kbesolve
+    return kbesolve
+
+
+def run_windows(workload, windows, K, workers=None, emit=None):
+    """Returns (per-step records, worst-case summary); emit(record) is called as they come."""
+    ref = reference()
+    emit = emit or (lambda rec: None)
+    cfg = dict(bench.WORKLOADS[workload])
     n_k, N, dt = cfg["n_k"], cfg["n_steps"], cfg["dt"]
     kw = bench.model_kwargs(cfg)
-    windows = [int(x) for x in os.environ.get("KBE_WINDOWS", "745,870,995").split(",")]
-    K = int(os.environ.get("KBE_WINDOW_STEPS", "5"))
-    workers = int(os.environ.get("KBE_REF_WORKERS", str(os.cpu_count() or 8)))
+    workers = workers or int(os.environ.get("KBE_REF_WORKERS", str(os.cpu_count() or 8)))
     shards = max(d for d in range(1, min(workers, n_k) + 1) if n_k % d == 0)
 
     windows = sorted(min(m, N - K) for m in windows)
@@ -70,10 +79,10 @@ def main():
     rdrv = ref.PropagationDriver(ref.build_kgrid(n_k), ref.ModelConfig(**kw),
                                  ref.StepConfig(dt=dt, n_steps=n_ref, memory_budget=1 << 44),
                                  ref.Schedule(n_shards=shards, workers=workers), ref.WorkerPool(workers))
-    print(json.dumps({"workload": cfg["workload"], "windows": windows, "steps_per_window": K,
-                      "ref_capacity": n_ref, "ref_workers": workers, "ref_shards": shards,
-                      "incremental": gdrv.ws.g_sh is not None}), flush=True)
-    worst = {}
+    emit({"workload": cfg["workload"], "windows": windows, "steps_per_window": K,
+          "ref_capacity": n_ref, "ref_workers": workers, "ref_shards": shards,
+          "incremental": gdrv.ws.g_sh is not None})
+    worst, records = {"iteration_flips": 0}, []
     for m in windows:
         while gdrv.state.frontier < m:
             gdrv.step()
@@ -117,13 +126,21 @@ def main():
             }
             if n == gpu[0][0]:
                 rec["state_handoff_seconds"] = round(t_load, 1)
-            worst["iteration_flips"] = worst.get("iteration_flips", 0) + int(gr.iterations != rr.iterations)
+            worst["iteration_flips"] += int(gr.iterations != rr.iterations)
             for k_ in ("row_lesser", "col_greater", "sigma_row_greater", "sigma_col_lesser",
                        "density_abs", "drift_abs"):
                 worst[k_] = max(worst.get(k_, 0.0), rec[k_])
-            print(json.dumps(rec), flush=True)
-    print(json.dumps({"summary": "max over all window steps", **worst,
-                      "final_step": gdrv.state.frontier}), flush=True)
+            records.append(rec)
+            emit(rec)
+    summary = {"summary": "max over all window steps", **worst, "final_step": gdrv.state.frontier}
+    emit(summary)
+    return records, summary
+
+
+def main():
+    windows = [int(x) for x in os.environ.get("KBE_WINDOWS", "745,870,995").split(",")]
+    run_windows(os.environ.get("KBE_WORKLOAD", "cfg3"), windows, int(os.environ.get("KBE_WINDOW_STEPS", "5")),
+                emit=lambda rec: print(json.dumps(rec), flush=True))
 
 
 if __name__ == "__main__":

@@ -111,3 +111,26 @@ def test_long_reference_golden_dmma_sigma(name, monkeypatch):
     """The same long runs with K1 on the FP64 tensor cores (sigma_dft_kernel)."""
     monkeypatch.setenv("KBE_SIGMA", "dft")
     _check(compare_long_golden(name))
+
+
+def test_cfg3_last_steps_continued_by_the_reference():
+    """The end of the north_star target itself: the GPU path runs cfg3 (n_k = 64, the
+    bench's seeded tables) to step 998, hands its whole state (G and Sigma blocks
+    [0..998]) to the UNMODIFIED reference (kbesolve from baseline/_ref, the driver's
+    offline install), and both take steps 999 and 1000 (tests/golden/late_windows.py;
+    the committed cfg3 golden covers the prefix from the ground state).  Skipped where the
+    reference is not installed."""
+    import sys
+    sys.path.insert(0, GOLDEN)
+    import late_windows as LW
+    try:
+        LW.reference()
+    except ImportError:
+        pytest.skip("the reference install (baseline/_ref) is absent")
+    recs, worst = LW.run_windows("cfg3", [998], 2)
+    print(json.dumps(worst))
+    assert [r["step"] for r in recs] == [999, 1000]
+    for key in ("row_lesser", "col_greater", "sigma_row_greater", "sigma_col_lesser", "drift_abs"):
+        assert worst[key] <= 1e-10, (key, worst)
+    assert worst["density_abs"] <= 1e-12, worst
+    assert worst["iteration_flips"] <= 1, worst
