@@ -110,11 +110,11 @@ typedef struct kbe_problem {
     void* s_sh;           /* [k_local][tri] complex64 shadow of the final Sigma slices */
     void* v_prev;         /* [k_local][2][8*plane_len(N)]: G and Sigma frontier of the last full evaluation */
     void* fcol_part;      /* [k_local][N+1][4]: column-direction sums of the frontier slice */
-    void* row_delta;      /* incremental evaluations' M_fp32 dv, same shapes as row_part, */
+    void* row_delta;      /* incremental evaluations' M_fp32 dv (complex64), shapes of row_part, */
     void* col_delta;      /* col_part and gc_part; K3 adds them to the full evaluation's  */
     void* gc_delta;       /* partials while the last evaluation was incremental          */
-    void* i_red;          /* [k_local][N+1][4]: I< rows (+ the diagonal) reduced by K3a (split K3) */
-    void* g_red;          /* [k_local][N+1][4]: I> columns reduced by K3a                           */
+    void* i_red;          /* [2][k_local][N+1][4]: I< rows (+ the diagonal) reduced by K3a (split K3); */
+    void* g_red;          /* I> columns likewise; [1] = the base sums of the last full evaluation  */
     /* peer-to-peer exchange over NVLink (p2p_world > 1; front_send / front_all are
      * then unused except for the initial slice): every rank owns a kbe_p2p_bytes()
      * buffer, opened by every peer through kbe_p2p_export / kbe_p2p_open. */

@@ -1227,6 +1227,14 @@ __device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
 __device__ __forceinline__ void st_keep2(cplx* p, cplx v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
+// the incremental evaluations' delta slots are complex64 (their values are FP32 sums, so
+// storing them as FP32 is exact and halves the K2 -> K3 delta traffic)
+__device__ __forceinline__ void st_keep_f(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep2_f(fcx* p, fcx v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -1719,9 +1727,12 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
         if (lane == 0)
             for (int i = 0; i < STG && i < mr; ++i) issue(s0 + i, (gcount + i) % STG);
         double* outP = (double*)(part == 0 ? P.row_part : P.gc_part);
-        double* outD = (double*)(part == 0 ? P.row_delta : P.gc_delta);
+        float* outD = (float*)(part == 0 ? P.row_delta : P.gc_delta);
         auto put = [&](double* out, int s, double rr) {
             if ((lane & 3) == 0) st_keep(&out[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
+        };
+        auto putD = [&](int s, float rr) {
+            if ((lane & 3) == 0) st_keep_f(&outD[(((int64_t)kl * P.nbb + bc) * N1 + s) * 8 + (lane >> 2)], rr, pol_keep);
         };
         auto shadow_cell = [&](unsigned st, fcx* lo, fcx* up) {
             const fcx* f = reinterpret_cast<const fcx*>(stage(st));
@@ -1805,16 +1816,16 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 float v[8];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
-                put(outD, s, (double)warp_rs8(v, lane));
+                putD(s, warp_rs8(v, lane));
             }
             };
             if (wb0 + TB <= s0) loop0(std::true_type{});
             else loop0(std::false_type{});
             // history-part column sums -> the chunk's delta slot
             if (b <= s1) {
-                cplx* colD = (cplx*)P.col_delta + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
+                fcx* colD = (fcx*)P.col_delta + (((int64_t)kl * P.nsb + s0 / ts) * N1 + b) * 4;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) st_keep2(&colD[c], cneg(f64(col[c])), pol_keep);
+                for (int c = 0; c < 4; ++c) st_keep2_f(&colD[c], make_float2(-col[c].x, -col[c].y), pol_keep);
             }
             if (s1 == n) {
                 // slice n in FP64 with the full vectors: base row slot (zero delta), fcol slot
@@ -1843,7 +1854,7 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 for (int c = 0; c < 4; ++c) { v[2 * c] = row[c].x; v[2 * c + 1] = row[c].y; }
                 const double rr = warp_rs8(v, lane);
                 put(outP, n, rr);
-                put(outD, n, 0.0);
+                putD(n, 0.f);
                 if (b <= n) {
                     cplx* fc = (cplx*)P.fcol_part + ((int64_t)kl * N1 + b) * 4;
 #pragma unroll
@@ -1900,7 +1911,7 @@ __device__ __forceinline__ void coll_body_incr(const kbe_problem& P, kbe_ctl* ct
                 float v[8];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) { v[2 * c] = acc[c].x; v[2 * c + 1] = acc[c].y; }
-                put(outD, j, (double)warp_rs8(v, lane));
+                putD(j, warp_rs8(v, lane));
             }
             };
             if (off) loop1(std::true_type{});
@@ -2189,12 +2200,26 @@ __device__ __forceinline__ void reduce_chunks(const kbe_problem& P, const void* 
     }
 }
 // I<(t_nf, t_l) / I>(t_nf, t_l) (rows) and I>(t_j, t_nf) / I<(t_j, t_nf) (columns)
-// + the delta slots when the last evaluation was incremental (as-printed only)
+// + the delta slots when the last evaluation was incremental (as-printed only); the
+// delta slots are complex64, summed in the same chunk order as reduce_chunks
 __device__ __forceinline__ void add_deltas(const kbe_problem& P, const void* rowd, const void* cold, int kl, int l,
                                            int nf, cplx* out) {
     if (P.limit_mode || !P.ctl || !((const volatile kbe_ctl*)P.ctl)->incr_last) return;
+    const int64_t N1 = P.n_steps + 1;
+    const int ts = coll_ts(nf, P.k_hi - P.k_lo, 0);
     cplx d[4];
-    reduce_chunks(P, rowd, cold, kl, l, nf, d);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) d[c] = cz();
+    const fcx* rp = (const fcx*)rowd + ((int64_t)kl * P.nbb * N1 + l) * 4;
+    for (int bc = 0; bc <= l / TB; ++bc)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) d[c] = cadd(d[c], f64(rp[bc * N1 * 4 + c]));
+    if (cold) {
+        const fcx* cp = (const fcx*)cold + ((int64_t)kl * P.nsb * N1 + l) * 4;
+        for (int sc = l / ts; sc <= nf / ts; ++sc)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) d[c] = cadd(d[c], f64(cp[sc * N1 * 4 + c]));
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) out[c] = cadd(out[c], d[c]);
 }
@@ -2445,11 +2470,12 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
 // acc_a += sum of na slots at pa (stride st), acc_b += nb slots at pb (b stream optional:
 // nb = 0); with D, each slot adds its delta slot at the same offset from da / db
 template <int B, bool D>
-__device__ __forceinline__ void red_streams(const cplx* pa, const cplx* da, int na, const cplx* pb, const cplx* db,
+__device__ __forceinline__ void red_streams(const cplx* pa, const fcx* da, int na, const cplx* pb, const fcx* db,
                                             int nb, int64_t st, cplx& acc_a, cplx& acc_b) {
     const int nmax = na > nb ? na : nb;
     for (int q = 0; q < nmax; q += B) {
-        cplx va[B], vb[B], wa[B], wb[B];
+        cplx va[B], vb[B];
+        fcx wa[B], wb[B];
         // every load of the batch is issued unconditionally (index clamped, value masked
         // afterwards): a branch around a load would serialise the batch
 #pragma unroll
@@ -2462,12 +2488,37 @@ __device__ __forceinline__ void red_streams(const cplx* pa, const cplx* da, int 
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            if (D) { va[u] = cadd(va[u], wa[u]); vb[u] = cadd(vb[u], wb[u]); }
+            if (D) { va[u] = cadd(va[u], f64(wa[u])); vb[u] = cadd(vb[u], f64(wb[u])); }
             if (q + u < na) acc_a = cadd(acc_a, va[u]);
             if (q + u < nb) acc_b = cadd(acc_b, vb[u]);
         }
     }
 }
+// the delta slots alone (complex64, summed in FP64): acc_a += na slots at da, acc_b += nb at db
+template <int B>
+__device__ __forceinline__ void red_streams_f(const fcx* da, int na, const fcx* db, int nb, int64_t st, cplx& acc_a,
+                                              cplx& acc_b) {
+    const int nmax = na > nb ? na : nb;
+    for (int q = 0; q < nmax; q += B) {
+        fcx wa[B], wb[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            wa[u] = __ldcg(da + (int64_t)min(q + u, na > 0 ? na - 1 : 0) * st);
+            wb[u] = __ldcg(db + (int64_t)min(q + u, nb > 0 ? nb - 1 : 0) * st);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (q + u < na) acc_a = cadd(acc_a, f64(wa[u]));
+            if (q + u < nb) acc_b = cadd(acc_b, f64(wb[u]));
+        }
+    }
+}
+// Incremental problems (INC): after a full evaluation K3a also keeps each point's sums
+// (before the frontier slot fcol) in the second half of i_red / g_red; after an
+// incremental evaluation at the same frontier only the delta slots changed for points
+// b < nf, so it reads those base sums and the (complex64) delta slots, not the base slots
+// again -- a third of the bytes.  Point nf (whose row slots the incremental evaluation
+// rewrites in FP64) keeps the slot-by-slot sum.
 template <int INC>
 __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
@@ -2500,11 +2551,14 @@ __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, in
             const cplx* gcP = (const cplx*)P.gc_part + rb;
             const cplx* colP = (const cplx*)P.col_part + cb;
             cplx dummy = cz();
-            if (INC && dl) {
-                red_streams<RED_BATCH / 2, true>(rowP, (const cplx*)P.row_delta + rb, mr, gcP,
-                                                 (const cplx*)P.gc_delta + rb, mg, st, a, gg);
-                red_streams<RED_BATCH / 2, true>(colP, (const cplx*)P.col_delta + cb, ms, colP,
-                                                 (const cplx*)P.col_delta + cb, 0, st, a, dummy);
+            if (INC && dl && b < nf) {
+                red_streams_f<8>((const fcx*)P.row_delta + rb, mr, (const fcx*)P.gc_delta + rb, mg, st, a, gg);
+                red_streams_f<8>((const fcx*)P.col_delta + cb, ms, (const fcx*)P.col_delta + cb, 0, st, a, dummy);
+            } else if (INC && dl) {
+                red_streams<RED_BATCH / 2, true>(rowP, (const fcx*)P.row_delta + rb, mr, gcP,
+                                                 (const fcx*)P.gc_delta + rb, mg, st, a, gg);
+                red_streams<RED_BATCH / 2, true>(colP, (const fcx*)P.col_delta + cb, ms, colP,
+                                                 (const fcx*)P.col_delta + cb, 0, st, a, dummy);
             } else {
                 red_streams<RED_BATCH, false>(rowP, nullptr, mr, gcP, nullptr, mg, st, a, gg);
                 red_streams<RED_BATCH, false>(colP, nullptr, ms, colP, nullptr, 0, st, a, dummy);
@@ -2520,6 +2574,17 @@ __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, in
         }
         if (b < npts && g == 0) {
             const int64_t oo = ((int64_t)kl * N1 + b) * 4 + c;
+            if (INC) {
+                cplx* bi = (cplx*)P.i_red + (int64_t)nkl * N1 * 4;   // base sums (second half)
+                cplx* bg = (cplx*)P.g_red + (int64_t)nkl * N1 * 4;
+                if (!dl) {
+                    bi[oo] = a;
+                    bg[oo] = gg;
+                } else if (b < nf) {
+                    a = cadd(__ldcg(bi + oo), a);
+                    gg = cadd(__ldcg(bg + oo), gg);
+                }
+            }
             if (b < nf) a = cadd(a, __ldcg((const cplx*)P.fcol_part + oo));
             ((cplx*)P.i_red)[oo] = a;
             ((cplx*)P.g_red)[oo] = gg;
@@ -2626,9 +2691,9 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
         cplx a = cz(), g = cz();
         // after an incremental evaluation every slot is base + delta (collision_kernel)
         const bool dl = INC && !LANG && ((const volatile kbe_ctl*)ctl)->incr_last;
-        const cplx* rowD = dl ? (const cplx*)P.row_delta + rb : nullptr;
-        const cplx* colD = dl ? (const cplx*)P.col_delta + cb : nullptr;
-        const cplx* gcD = dl ? (const cplx*)P.gc_delta + rb : nullptr;
+        const fcx* rowD = dl ? (const fcx*)P.row_delta + rb : nullptr;
+        const fcx* colD = dl ? (const fcx*)P.col_delta + cb : nullptr;
+        const fcx* gcD = dl ? (const fcx*)P.gc_delta + rb : nullptr;
         for (int i0 = 0; i0 < na || i0 < ng; i0 += UPD_BATCH) {
             cplx va[UPD_BATCH], vg[UPD_BATCH];
 #pragma unroll
@@ -2637,8 +2702,8 @@ __global__ void __launch_bounds__(512) update_kernel(kbe_problem P, int n, int p
                 va[u] = q < na ? (q < nr ? rowP[q * cs] : colP[(c0 + q - nr) * cs]) : cz();
                 vg[u] = q < ng ? (q < nr ? gcP[q * cs] : gcC[(c0 + q - nr) * cs]) : cz();
                 if (dl) {
-                    if (q < na) va[u] = cadd(va[u], q < nr ? rowD[q * cs] : colD[(c0 + q - nr) * cs]);
-                    if (q < ng) vg[u] = cadd(vg[u], gcD[q * cs]);
+                    if (q < na) va[u] = cadd(va[u], f64(q < nr ? rowD[q * cs] : colD[(c0 + q - nr) * cs]));
+                    if (q < ng) vg[u] = cadd(vg[u], f64(gcD[q * cs]));
                 }
             }
 #pragma unroll

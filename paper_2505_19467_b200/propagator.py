@@ -175,8 +175,10 @@ class _Workspace:
         self.phi = torch.zeros((N1, kl, 4), **c128)
         self.fcol_part = torch.zeros((kl, N1, 4), **c128)
         # K3a -> K3b hand-off of the split update (as-printed, many local k)
-        self.i_red = torch.zeros((kl, N1, 4), **c128)
-        self.g_red = torch.zeros((kl, N1, 4), **c128)
+        # [0]: the sums K3b reads; [1]: incremental problems' base sums of the last full
+        # evaluation (reduce_kernel)
+        self.i_red = torch.zeros((2, kl, N1, 4), **c128)
+        self.g_red = torch.zeros((2, kl, N1, 4), **c128)
         # incremental collision evaluations (as-printed): complex64 shadows of the final
         # history slices and the frontier the last evaluation used (include/kbe200.h)
         self.g_sh = self.s_sh = self.v_prev = None
@@ -184,7 +186,9 @@ class _Workspace:
             self.g_sh = torch.zeros_like(g_hist, dtype=torch.complex64)
             self.s_sh = torch.zeros_like(s_hist, dtype=torch.complex64)
             self.v_prev = torch.zeros((kl, 2, 8 * _lib.plane_len(n_steps)), **c128)
-            self.deltas = [torch.zeros_like(t) for t in (self.row_part, self.col_part, self.gc_part)]
+            # delta slots: complex64 (FP32 sums, stored exactly; kbe200.cu st_keep_f)
+            self.deltas = [torch.zeros(t.shape, dtype=torch.complex64, device=device)
+                           for t in (self.row_part, self.col_part, self.gc_part)]
         self.lang = None
         if limit_mode:   # langreth: I> rows and I< columns kept separately, both directions
             shapes = (self.nbb, self.nsb, self.nbb, self.nsb, self.nsb)   # row_g, col_g, lc, gc_c, lc_c

@@ -1,11 +1,14 @@
 """Isolated K2 timing, full vs incremental evaluation, at one frontier.
 
-    python profiles/incr_ab.py [--workload cfg2] [--n 900] [--reps 20] [--ncu full|incr]
+    python profiles/incr_ab.py [--workload cfg2] [--n 900] [--reps 20] [--ncu full|incr] [--update]
 
 Propagates to step n-1, runs step n's predictor and first corrector, then times
 repeated corrector-1 collision launches at frontier n with the iteration-0 residual
 forced to 1e-3 (full FP64 evaluation) and to 2e-9 (incremental: complex64 history
 shadow + FP64 frontier slice).  Timing only: the forced residual is not physical.
+--update also times the corrector update that consumes each kind of evaluation
+(kbe_update: K3a reduce + K3b update at >= 8 local k), re-launched after one collision
+launch of that kind.
 """
 
 from __future__ import annotations
@@ -32,6 +35,7 @@ def main():
     ap.add_argument("--ncu", choices=["full", "incr"], default=None,
                     help="bracket one launch of that mode with cudaProfilerStart/Stop "
                          "(ncu --profile-from-start off); no timing")
+    ap.add_argument("--update", action="store_true")
     args = ap.parse_args()
     cfgw = bench.select_workload(args.workload)
     import paper_2505_19467_b200 as kb
@@ -82,6 +86,21 @@ def main():
     out = {"workload": args.workload, "n": n, "lib": os.environ.get("KBE_LIB", "product")}
     out["full_us"] = timed(1e-3)
     out["incr_us"] = timed(2e-9)   # > eps (not converged); 23 launches accumulate 4.6e-8 <= KBE_INCR_MAX_DELTA
+    if args.update:
+        def timed_update(r0):
+            res[0] = struct.unpack("<q", struct.pack("<d", r0))[0]
+            _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+            for _ in range(3):
+                _lib.check(L.kbe_update(P, n, 1, 1, sp))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(args.reps):
+                _lib.check(L.kbe_update(P, n, 1, 1, sp))
+            e1.record(st)
+            torch.cuda.synchronize()
+            return 1e3 * e0.elapsed_time(e1) / args.reps
+        out["update_after_full_us"] = timed_update(1e-3)
+        out["update_after_incr_us"] = timed_update(2e-9)
     out["full_gbs"] = full_b / (out["full_us"] * 1e-6) / 1e9
     out["incr_gbs"] = incr_b / (out["incr_us"] * 1e-6) / 1e9
     print(json.dumps(out))
