@@ -2457,123 +2457,84 @@ __device__ __forceinline__ void publish_tail(const kbe_problem& P, const KbeTail
 //   g(b) = sum_{bc <= b/TB} gc[bc][b]                                         (b < nf)
 // (+ the delta slots after an incremental evaluation); points 0..n-1, and n itself in
 // the corrector (the diagonal's I<(t_n, t_n)).
-// One warp item = 2 points x 4 block entries of one local k (8 outputs, 128 contiguous
-// bytes per slot) x RED_G slot groups: lane g*8 + o sums, in order, the row slots
-// bc = g, g + RED_G, ... (< b/TB + 1) and then the column slots sc = b/ts + g, ... of a(b),
-// and the gc slots bc = g, ... of g(b); the groups are combined by a fixed xor-shuffle
-// tree.  Each stream is a strided pointer walk with RED_BATCH loads in flight (the row
-// and gc streams interleaved), so the loop is loads and adds only.  The summation order
-// depends only on (n, b): results are bitwise reproducible and independent of the
-// launch shape.  Persistent grid, items strided over all warps.
-#define RED_G 4
-#define RED_BATCH 6
-// acc_a += sum of na slots at pa (stride st), acc_b += nb slots at pb (b stream optional:
-// nb = 0); with D, each slot adds its delta slot at the same offset from da / db
-template <int B, bool D>
-__device__ __forceinline__ void red_streams(const cplx* pa, const fcx* da, int na, const cplx* pb, const fcx* db,
-                                            int nb, int64_t st, cplx& acc_a, cplx& acc_b) {
-    const int nmax = na > nb ? na : nb;
-    for (int q = 0; q < nmax; q += B) {
-        cplx va[B], vb[B];
-        fcx wa[B], wb[B];
-        // every load of the batch is issued unconditionally (index clamped, value masked
-        // afterwards): a branch around a load would serialise the batch
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            const int64_t ia = (int64_t)min(q + u, na > 0 ? na - 1 : 0) * st;
-            const int64_t ib = (int64_t)min(q + u, nb > 0 ? nb - 1 : 0) * st;
-            va[u] = __ldcg(pa + ia);
-            vb[u] = __ldcg(pb + ib);
-            if (D) { wa[u] = __ldcg(da + ia); wb[u] = __ldcg(db + ib); }
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            if (D) { va[u] = cadd(va[u], f64(wa[u])); vb[u] = cadd(vb[u], f64(wb[u])); }
-            if (q + u < na) acc_a = cadd(acc_a, va[u]);
-            if (q + u < nb) acc_b = cadd(acc_b, vb[u]);
-        }
-    }
-}
-// the delta slots alone (complex64, summed in FP64): acc_a += na slots at da, acc_b += nb at db
-template <int B>
-__device__ __forceinline__ void red_streams_f(const fcx* da, int na, const fcx* db, int nb, int64_t st, cplx& acc_a,
-                                              cplx& acc_b) {
-    const int nmax = na > nb ? na : nb;
-    for (int q = 0; q < nmax; q += B) {
-        fcx wa[B], wb[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            wa[u] = __ldcg(da + (int64_t)min(q + u, na > 0 ? na - 1 : 0) * st);
-            wb[u] = __ldcg(db + (int64_t)min(q + u, nb > 0 ? nb - 1 : 0) * st);
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            if (q + u < na) acc_a = cadd(acc_a, f64(wa[u]));
-            if (q + u < nb) acc_b = cadd(acc_b, f64(wb[u]));
-        }
-    }
-}
+// One warp item = 8 consecutive points x 4 block entries of one local k; lane
+// 4*(b - b0) + c owns output (b, c), so every slot is one coalesced 512-byte warp load.
+// Aligned groups of 8 points share their slot counts (TB = 32 and the column chunk
+// ts in {8, 16, 32} are multiples of 8), so the loop bounds are warp-uniform and each
+// lane sums its own slots in order -- row slots bc = 0 .. b/TB (the gc slots at the same
+// offsets), and column chunks sc = b/ts .. nf/ts, as (row sum) + (column sum) + fcol --
+// all three streams in one batched loop, no shuffles (round-2 v1 split every point's slots over
+// 4 lane groups and clamped every load: 720 warp instructions per item, issue-bound at
+// 67 us for cfg3 n = 900, profiles/r02/final2/k3a_*_v1_*).  The summation order depends
+// only on (n, b): results are bitwise reproducible and independent of the launch shape.
 // Incremental problems (INC): after a full evaluation K3a also keeps each point's sums
-// (before the frontier slot fcol) in the second half of i_red / g_red; after an
-// incremental evaluation at the same frontier only the delta slots changed for points
-// b < nf, so it reads those base sums and the (complex64) delta slots, not the base slots
-// again -- a third of the bytes.  Point nf (whose row slots the incremental evaluation
-// rewrites in FP64) keeps the slot-by-slot sum.
+// (before fcol) in the second half of i_red / g_red; after an incremental evaluation at
+// the same frontier only the delta slots changed for points b < nf, so it reads those
+// sums and the complex64 delta slots, not the base slots again.  Point nf (whose row
+// slots the incremental evaluation rewrites in FP64) sums base and delta slots.
+// Persistent grid, items strided over all warps.
+__device__ __forceinline__ cplx as_c128(cplx v) { return v; }
+__device__ __forceinline__ cplx as_c128(fcx v) { return f64(v); }
+// the row (pr) and gc (pg) streams of nr slots and the column stream (pc) of nc slots in
+// one loop: each batch has all three streams' loads in flight (the loop is load-latency
+// bound); ar += row slots, g += gc slots, ac += column slots, each in slot order
+template <int B, class T>
+__device__ __forceinline__ void sum_slots3(const T* pr, const T* pg, int nr, const T* pc, int nc, int64_t st,
+                                           cplx& ar, cplx& g, cplx& ac) {
+    const int nmax = nr > nc ? nr : nc;
+    for (int q = 0; q < nmax; q += B) {
+        T vr[B], vg[B], vc[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int64_t o = (int64_t)min(q + u, nr - 1) * st;
+            vr[u] = __ldcg(pr + o);
+            vg[u] = __ldcg(pg + o);
+            vc[u] = __ldcg(pc + (int64_t)min(q + u, nc - 1) * st);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (q + u < nr) {
+                ar = cadd(ar, as_c128(vr[u]));
+                g = cadd(g, as_c128(vg[u]));
+            }
+            if (q + u < nc) ac = cadd(ac, as_c128(vc[u]));
+        }
+    }
+}
 template <int INC>
 __global__ void __launch_bounds__(256, 3) reduce_kernel(kbe_problem P, int n, int phase, int it) {
     pdl_enter();
     const kbe_ctl* ctl = (const kbe_ctl*)P.ctl;
     if (phase == 0 ? kbe_halted(ctl) : kbe_skip(P, ctl, it)) return;
     const int nkl = P.k_hi - P.k_lo;
-    const int64_t N1 = P.n_steps + 1, cs = N1 * 4, st = cs * RED_G;
+    const int64_t N1 = P.n_steps + 1, cs = N1 * 4;
     const int nf = phase == 0 ? n - 1 : n;
-    const int npts = phase == 0 ? n : n + 1;
+    const int npts = nf + 1;
     const int cts = coll_ts(nf, nkl, 0);
     const bool dl = INC && ((const volatile kbe_ctl*)ctl)->incr_last;
-    const int lane = threadIdx.x & 31, g = lane >> 3, o = lane & 7;
-    const int pairs = (npts + 1) >> 1;
-    const int items = nkl * pairs;
+    const int lane = threadIdx.x & 31, c = lane & 3;
+    const int groups = (npts + 7) >> 3;
+    const int items = nkl * groups;
     const int warps = gridDim.x * (blockDim.x >> 5);
     for (int item = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < items; item += warps) {
-        const int kl = item / pairs;
-        const int b = (item % pairs) * 2 + (o >> 2), c = o & 3;
-        cplx a = cz(), gg = cz();
+        const int kl = item / groups, b0 = (item % groups) * 8;
+        const int b = b0 + (lane >> 2);
+        const int bl = min(b, nf);   // lanes past the frontier load point nf's slots (no store)
+        const int nr = b0 / TB + 1, c0 = b0 / cts, ns = nf / cts - c0 + 1;   // warp-uniform
+        const int64_t rb = ((int64_t)kl * P.nbb * N1 + bl) * 4 + c;
+        const int64_t cb = ((int64_t)kl * P.nsb * N1 + bl) * 4 + c + (int64_t)c0 * cs;
+        // a = (row slots) + (column slots), each summed in slot order
+        cplx ar = cz(), ac = cz(), gg = cz();
+        if (INC && dl)
+            sum_slots3<6>((const fcx*)P.row_delta + rb, (const fcx*)P.gc_delta + rb, nr,
+                          (const fcx*)P.col_delta + cb, ns, cs, ar, gg, ac);
+        if (!(INC && dl) || bl == nf)
+            sum_slots3<4>((const cplx*)P.row_part + rb, (const cplx*)P.gc_part + rb, nr,
+                          (const cplx*)P.col_part + cb, ns, cs, ar, gg, ac);
+        cplx a = cadd(ar, ac);
         if (b < npts) {
-            const int64_t rb = ((int64_t)kl * P.nbb * N1 + b) * 4 + c + g * cs;
-            const int c0 = b / cts;
-            const int64_t cb = ((int64_t)kl * P.nsb * N1 + b) * 4 + c + (int64_t)(c0 + g) * cs;
-            const int nr = b / TB + 1, ns = nf / cts - c0 + 1;
-            // slots of this lane's group
-            const int mr = nr > g ? (nr - g + RED_G - 1) / RED_G : 0;
-            const int ms = ns > g ? (ns - g + RED_G - 1) / RED_G : 0;
-            const int mg = b < nf ? mr : 0;
-            const cplx* rowP = (const cplx*)P.row_part + rb;
-            const cplx* gcP = (const cplx*)P.gc_part + rb;
-            const cplx* colP = (const cplx*)P.col_part + cb;
-            cplx dummy = cz();
-            if (INC && dl && b < nf) {
-                red_streams_f<8>((const fcx*)P.row_delta + rb, mr, (const fcx*)P.gc_delta + rb, mg, st, a, gg);
-                red_streams_f<8>((const fcx*)P.col_delta + cb, ms, (const fcx*)P.col_delta + cb, 0, st, a, dummy);
-            } else if (INC && dl) {
-                red_streams<RED_BATCH / 2, true>(rowP, (const fcx*)P.row_delta + rb, mr, gcP,
-                                                 (const fcx*)P.gc_delta + rb, mg, st, a, gg);
-                red_streams<RED_BATCH / 2, true>(colP, (const fcx*)P.col_delta + cb, ms, colP,
-                                                 (const fcx*)P.col_delta + cb, 0, st, a, dummy);
-            } else {
-                red_streams<RED_BATCH, false>(rowP, nullptr, mr, gcP, nullptr, mg, st, a, gg);
-                red_streams<RED_BATCH, false>(colP, nullptr, ms, colP, nullptr, 0, st, a, dummy);
-            }
-        }
-        // groups (lanes o, o+8, o+16, o+24): ((g0 + g1) + (g2 + g3)); a + b == b + a exactly
-#pragma unroll
-        for (int off = 8; off < 32; off <<= 1) {
-            a.x += __shfl_xor_sync(0xffffffffu, a.x, off);
-            a.y += __shfl_xor_sync(0xffffffffu, a.y, off);
-            gg.x += __shfl_xor_sync(0xffffffffu, gg.x, off);
-            gg.y += __shfl_xor_sync(0xffffffffu, gg.y, off);
-        }
-        if (b < npts && g == 0) {
             const int64_t oo = ((int64_t)kl * N1 + b) * 4 + c;
+            if (b == nf) gg = cz();   // no gc slots for the frontier point
             if (INC) {
                 cplx* bi = (cplx*)P.i_red + (int64_t)nkl * N1 * 4;   // base sums (second half)
                 cplx* bg = (cplx*)P.g_red + (int64_t)nkl * N1 * 4;
@@ -3385,7 +3346,7 @@ static bool upd_split(const kbe_problem* p) {
     return !p->limit_mode && p->i_red && p->g_red && (p->k_hi - p->k_lo) >= g_split_min_k;
 }
 static void spec_reduce(KSpec& s, const kbe_problem* p, int n, int phase, int it) {
-    const int64_t items = (int64_t)(p->k_hi - p->k_lo) * (((phase == 0 ? n : n + 1) + 1) / 2);
+    const int64_t items = (int64_t)(p->k_hi - p->k_lo) * (((phase == 0 ? n : n + 1) + 7) / 8);
     const int64_t cap = (int64_t)g_num_sms * 3;   // resident CTAs (__launch_bounds__(256, 3))
     const dim3 grid((unsigned)std::min<int64_t>((items + 7) / 8, cap));
     if (p->g_sh) make_spec(s, reduce_kernel<1>, grid, dim3(256), 0, *p, n, phase, it);

@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--n", type=int, default=900)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--ncu", choices=["full", "incr"], default=None,
+    ap.add_argument("--ncu", choices=["full", "incr", "full_update", "incr_update"], default=None,
                     help="bracket one launch of that mode with cudaProfilerStart/Stop "
                          "(ncu --profile-from-start off); no timing")
     ap.add_argument("--update", action="store_true")
@@ -70,12 +70,19 @@ def main():
         return 1e3 * e0.elapsed_time(e1) / args.reps
 
     if args.ncu:
-        res[0] = struct.unpack("<q", struct.pack("<d", 1e-3 if args.ncu == "full" else 2e-9))[0]
+        # *_update: bracket the update (K3a + K3b) that consumes one evaluation of that kind
+        upd = args.ncu.endswith("_update")
+        res[0] = struct.unpack("<q", struct.pack("<d", 1e-3 if args.ncu.startswith("full") else 2e-9))[0]
         for _ in range(3):
             _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        if upd:
+            _lib.check(L.kbe_update(P, n, 1, 1, sp))
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
-        _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
+        if upd:
+            _lib.check(L.kbe_update(P, n, 1, 1, sp))
+        else:
+            _lib.check(L.kbe_collision_frontier(P, n, 1, sp))
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
         return
