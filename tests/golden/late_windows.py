@@ -20,7 +20,9 @@ Test infrastructure only (runs where baseline/_ref and a GPU exist, i.e. the GPU
         > gpurun_out/late_windows.jsonl
 
 KBE_WINDOWS (default "745,870,995") and KBE_WINDOW_STEPS (default 5) choose the windows;
-KBE_WORKLOAD another bench workload (e.g. cfg1 with KBE_WINDOWS=150 for a quick check).
+KBE_WORKLOAD another bench workload (e.g. cfg1 with KBE_WINDOWS=150 for a quick check);
+KBE_STEP_OPTS / KBE_MODEL_OPTS (JSON) the non-default physics, e.g.
+KBE_STEP_OPTS='{"quadrature": "simpson"}'.
 """
 
 from __future__ import annotations
@@ -57,13 +59,17 @@ def reference():
     return kbesolve
 
 
-def run_windows(workload, windows, K, workers=None, emit=None):
-    """Returns (per-step records, worst-case summary); emit(record) is called as they come."""
+def run_windows(workload, windows, K, workers=None, emit=None, step_opts=None, model_opts=None):
+    """Returns (per-step records, worst-case summary); emit(record) is called as they come.
+    step_opts / model_opts: extra StepConfig / ModelConfig fields for both sides (the
+    non-default physics: quadrature="simpson", limit_mode="langreth", hf_mode="on")."""
+    step_opts, model_opts = dict(step_opts or {}), dict(model_opts or {})
     ref = reference()
     emit = emit or (lambda rec: None)
     cfg = dict(bench.WORKLOADS[workload])
     n_k, N, dt = cfg["n_k"], cfg["n_steps"], cfg["dt"]
     kw = bench.model_kwargs(cfg)
+    kw.update(model_opts)
     workers = workers or int(os.environ.get("KBE_REF_WORKERS", str(os.cpu_count() or 8)))
     shards = max(d for d in range(1, min(workers, n_k) + 1) if n_k % d == 0)
 
@@ -74,12 +80,12 @@ def run_windows(workload, windows, K, workers=None, emit=None):
     n_ref = max(windows) + K
     torch.cuda.set_device(0)
     gdrv = kb.PropagationDriver(kb.build_kgrid(n_k), kb.ModelConfig(**kw),
-                                kb.StepConfig(dt=dt, n_steps=N, memory_budget=1 << 40))
+                                kb.StepConfig(dt=dt, n_steps=N, memory_budget=1 << 40, **step_opts))
     sig = TwoTimeGF(n_k, 0, N, dt, gdrv.sigma.hist)          # Sigma history, same packing
     rdrv = ref.PropagationDriver(ref.build_kgrid(n_k), ref.ModelConfig(**kw),
-                                 ref.StepConfig(dt=dt, n_steps=n_ref, memory_budget=1 << 44),
+                                 ref.StepConfig(dt=dt, n_steps=n_ref, memory_budget=1 << 44, **step_opts),
                                  ref.Schedule(n_shards=shards, workers=workers), ref.WorkerPool(workers))
-    emit({"workload": cfg["workload"], "windows": windows, "steps_per_window": K,
+    emit({"workload": cfg["workload"], "step_opts": step_opts, "model_opts": model_opts, "windows": windows, "steps_per_window": K,
           "ref_capacity": n_ref, "ref_workers": workers, "ref_shards": shards,
           "incremental": gdrv.ws.g_sh is not None})
     worst, records = {"iteration_flips": 0}, []
@@ -140,7 +146,9 @@ def run_windows(workload, windows, K, workers=None, emit=None):
 def main():
     windows = [int(x) for x in os.environ.get("KBE_WINDOWS", "745,870,995").split(",")]
     run_windows(os.environ.get("KBE_WORKLOAD", "cfg3"), windows, int(os.environ.get("KBE_WINDOW_STEPS", "5")),
-                emit=lambda rec: print(json.dumps(rec), flush=True))
+                emit=lambda rec: print(json.dumps(rec), flush=True),
+                step_opts=json.loads(os.environ.get("KBE_STEP_OPTS", "{}")),
+                model_opts=json.loads(os.environ.get("KBE_MODEL_OPTS", "{}")))
 
 
 if __name__ == "__main__":
